@@ -1,0 +1,589 @@
+"""CPU oracle for the DDF path-tracing hot path.  TEST INFRASTRUCTURE ONLY.
+
+This module is the checker, never the product: only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import it.  The shipped path
+(``paper_2306_16142_b200``) never imports it and has no CPU fallback.
+
+It is a float64 numpy restatement of the reference's hot path
+(``/root/reference/pkg/src/ddfield``; paths below are relative to that
+package).  Every function cites the reference lines it follows.  Where the
+BASELINE configs ask for things the reference cannot express (65-D positional
+encoding, Russian roulette, an 8-object min-composite scene) the restatement
+extends the reference the way SURVEY.md Appendix A specifies; those parts are
+marked EXTENSION and their parity is "parity with this restatement".
+
+Pinning: ``tests/golden/make_golden.py`` runs the unmodified reference (it is
+importable in the build container) and stores its outputs as fixtures;
+``tests/test_oracle_golden.py`` checks this module against every fixture, and
+against the live reference when ``/root/reference`` is present.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+TWO_PI = 2.0 * np.pi
+HIT_FRACTION = 0.98          # field.py:24  MISS_FRACTION
+EVAL_CHUNK = 262_144         # neural.py:135 _EVAL_CHUNK
+PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645   # numpy PCG64 (XSL-RR 128/64) multiplier
+M64 = (1 << 64) - 1
+M128 = (1 << 128) - 1
+RNG_TAG = 0x9A7              # render.py:209  default_rng([seed, 0x9A7])
+RR_TAG = 0x5252              # EXTENSION: independent Russian-roulette stream
+PE_OCTAVES = 6               # EXTENSION: configs 3-5 positional encoding
+
+
+class OracleDataError(Exception):
+    pass
+
+
+class OracleNumericError(Exception):
+    pass
+
+
+# --------------------------------------------------------------------------
+# weights (neural.py:41-95, 378-431)
+# --------------------------------------------------------------------------
+
+@dataclass
+class Net:
+    """One MLP as the reference stores it: V (out,in), g (out,), b (out,)."""
+    widths: tuple
+    v: list
+    g: list
+    b: list
+
+    def effective(self):
+        """neural.py:69-74  W = g * V / |V| row-wise, in float64."""
+        out = []
+        for v, g in zip(self.v, self.g):
+            nrm = np.linalg.norm(v, axis=1)
+            out.append(g[:, None] * v / nrm[:, None])
+        return out
+
+    @property
+    def encoding(self) -> str:
+        return "pe6" if self.widths[0] == 5 * (1 + 2 * PE_OCTAVES) else "raw5"
+
+
+def kaiming_uniform_net(widths, seed: int) -> Net:
+    """BASELINE configs' synthetic weights: per layer in
+    order, V ~ U(+-sqrt(6/fan_in)) of shape (out, in) from default_rng(seed),
+    g = |V| row norms (so W == V), b = 0."""
+    rng = np.random.default_rng(seed)
+    vs, gs, bs = [], [], []
+    for i in range(len(widths) - 1):
+        lim = np.sqrt(6.0 / widths[i])
+        v = rng.uniform(-lim, lim, size=(widths[i + 1], widths[i]))
+        vs.append(v)
+        gs.append(np.linalg.norm(v, axis=1))
+        bs.append(np.zeros(widths[i + 1]))
+    return Net(tuple(int(w) for w in widths), vs, gs, bs)
+
+
+def write_ddfn(net: Net, delta: float, path) -> None:
+    """DDFN v1 layout (neural.py:378-390)."""
+    blob = bytearray(b"DDFN")
+    blob += struct.pack("<II", 1, len(net.widths))
+    blob += struct.pack(f"<{len(net.widths)}I", *net.widths)
+    blob += struct.pack("<d", float(delta))
+    for v, g, b in zip(net.v, net.g, net.b):
+        for a in (v, g, b):
+            blob += np.ascontiguousarray(a, dtype="<f8").tobytes()
+    with open(path, "wb") as fh:
+        fh.write(bytes(blob))
+
+
+def read_ddfn(path):
+    """DDFN v1 reader with the reference's error cases (neural.py:393-431)."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if blob[:4] != b"DDFN":
+        raise OracleDataError("not a DDFN checkpoint")
+    try:
+        ver, nw = struct.unpack_from("<II", blob, 4)
+        if ver != 1:
+            raise OracleDataError(f"unsupported checkpoint version {ver}")
+        widths = struct.unpack_from(f"<{nw}I", blob, 12)
+        (delta,) = struct.unpack_from("<d", blob, 12 + 4 * nw)
+    except struct.error as exc:
+        raise OracleDataError("truncated checkpoint header") from exc
+    off = 20 + 4 * nw
+    vs, gs, bs = [], [], []
+    for i in range(nw - 1):
+        o, n = widths[i + 1], widths[i]
+        need = (o * n + 2 * o) * 8
+        if off + need > len(blob):
+            raise OracleDataError(f"truncated checkpoint (layer {i})")
+        arr = np.frombuffer(blob, "<f8", count=o * n + 2 * o, offset=off)
+        vs.append(arr[:o * n].reshape(o, n).copy())
+        gs.append(arr[o * n:o * n + o].copy())
+        bs.append(arr[o * n + o:].copy())
+        off += need
+    if off != len(blob):
+        raise OracleDataError(f"{len(blob) - off} trailing bytes in checkpoint")
+    return Net(tuple(widths), vs, gs, bs), float(delta)
+
+
+# --------------------------------------------------------------------------
+# angles and input encoding (field.py:69-112, neural.py:26-38)
+# --------------------------------------------------------------------------
+
+def dirs_to_angles(d):
+    """field.py:77-82  (azimuth mod 2pi, polar from +z)."""
+    d = np.atleast_2d(d)
+    pol = np.arccos(np.clip(d[:, 2], -1.0, 1.0))
+    az = np.arctan2(d[:, 1], d[:, 0]) % TWO_PI
+    return np.stack([az, pol], axis=1)
+
+
+def angles_to_dirs(a):
+    """field.py:69-74."""
+    a = np.atleast_2d(a)
+    s = np.sin(a[:, 1])
+    return np.stack([np.cos(a[:, 0]) * s, np.sin(a[:, 0]) * s, np.cos(a[:, 1])], axis=1)
+
+
+def encode5(pos, ang):
+    """neural.py:26-38: (x, y, z, az/pi - 1, 2*pol/pi - 1)."""
+    pos = np.atleast_2d(pos)
+    ang = np.atleast_2d(ang)
+    u = np.empty((len(pos), 5))
+    u[:, :3] = pos
+    u[:, 3] = ang[:, 0] / np.pi - 1.0
+    u[:, 4] = 2.0 * ang[:, 1] / np.pi - 1.0
+    return u
+
+
+def pe_encode(u):
+    """EXTENSION (configs 3-5): 65-D sin/cos encoding of the
+    five encoded inputs.  Column order (fixed, documented in DESIGN.md):
+    [u_0..u_4, then for k = 0..5: sin(2^k pi u_0..4), cos(2^k pi u_0..4)]."""
+    cols = [u]
+    for k in range(PE_OCTAVES):
+        arg = (2.0 ** k) * np.pi * u
+        cols.append(np.sin(arg))
+        cols.append(np.cos(arg))
+    return np.concatenate(cols, axis=1)
+
+
+def pe_chain(u, g65):
+    """EXTENSION: d out / d u through pe_encode, given d out / d(65 inputs)."""
+    g = g65[:, :5].copy()
+    for k in range(PE_OCTAVES):
+        f = (2.0 ** k) * np.pi
+        arg = f * u
+        base = 5 + 10 * k
+        g += f * np.cos(arg) * g65[:, base:base + 5]
+        g -= f * np.sin(arg) * g65[:, base + 5:base + 10]
+    return g
+
+
+def net_inputs(net: Net, u):
+    return pe_encode(u) if net.encoding == "pe6" else u
+
+
+# --------------------------------------------------------------------------
+# MLP forward and input gradient (neural.py:138-157, 229-249)
+# --------------------------------------------------------------------------
+
+def mlp_forward(net: Net, x, ws=None):
+    """neural.py:138-157 eval-mode forward: ReLU hidden layers, identity head,
+    EVAL_CHUNK-row slabs."""
+    x = np.atleast_2d(x)
+    ws = net.effective() if ws is None else ws
+    last = len(ws) - 1
+    out = np.empty(len(x))
+    for lo in range(0, len(x), EVAL_CHUNK):
+        h = x[lo:lo + EVAL_CHUNK]
+        for i, w in enumerate(ws):
+            h = h @ w.T + net.b[i]
+            if i != last:
+                np.maximum(h, 0.0, out=h)
+        out[lo:lo + EVAL_CHUNK] = h[:, 0]
+    return out
+
+
+def mlp_input_grad(net: Net, x, ws=None):
+    """neural.py:229-249 generalised to any input width (the reference
+    hard-codes 5 at neural.py:234): forward keeping ReLU masks, then
+    d_h <- (d_h * mask) @ W down to the inputs."""
+    x = np.atleast_2d(x)
+    ws = net.effective() if ws is None else ws
+    last = len(ws) - 1
+    out = np.empty((len(x), x.shape[1]))
+    for lo in range(0, len(x), EVAL_CHUNK):
+        h = x[lo:lo + EVAL_CHUNK]
+        masks = []
+        for i, w in enumerate(ws):
+            h = h @ w.T + net.b[i]
+            if i != last:
+                m = h > 0.0
+                masks.append(m)
+                h = h * m
+        dh = np.ones((len(h), 1))
+        for i in range(last, -1, -1):
+            dz = dh if i == last else dh * masks[i]
+            dh = dz @ ws[i]
+        out[lo:lo + EVAL_CHUNK] = dh
+    return out
+
+
+def net_predict(net: Net, pos, ang, ws=None):
+    """field.py:244-246 (_predict), plus the PE extension."""
+    return mlp_forward(net, net_inputs(net, encode5(pos, ang)), ws)
+
+
+def net_grad5(net: Net, pos, ang, ws=None):
+    """field.py:291-293 (input_gradients) -> (N,5), plus the PE extension."""
+    u = encode5(pos, ang)
+    if net.encoding == "pe6":
+        return pe_chain(u, mlp_input_grad(net, pe_encode(u), ws))
+    return mlp_input_grad(net, u, ws)
+
+
+# --------------------------------------------------------------------------
+# the field: query / trace / normal (field.py:218-337)
+# --------------------------------------------------------------------------
+
+def ray_box(o, d, lo, hi):
+    """field.py:323-337 vectorised slab test; enter > exit on a miss."""
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / d
+        t0 = (lo - o) * inv
+        t1 = (hi - o) * inv
+    a = np.minimum(t0, t1)
+    b = np.maximum(t0, t1)
+    z = d == 0.0
+    if z.any():
+        inside = (o >= lo) & (o <= hi)
+        a = np.where(z, np.where(inside, -np.inf, np.inf), a)
+        b = np.where(z, np.where(inside, np.inf, -np.inf), b)
+    return a.max(axis=1), b.min(axis=1)
+
+
+@dataclass
+class Field:
+    """A DDF backend: one network (the reference NeuralField, field.py:218-317)
+    or, EXTENSION for config 5, several networks composed by min with
+    per-object translation ``centers`` and uniform ``scale``."""
+    nets: list
+    delta: float
+    bounds: np.ndarray = dc_field(default_factory=lambda: np.array([[-1.1] * 3, [1.1] * 3]))
+    centers: np.ndarray | None = None
+    scale: float = 1.0
+    albedos: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.bounds = np.asarray(self.bounds, dtype=np.float64)
+        self._ws = [n.effective() for n in self.nets]
+        if self.centers is None:
+            self.centers = np.zeros((len(self.nets), 3))
+        self.centers = np.asarray(self.centers, dtype=np.float64)
+        self.normal_eval_backoff = 0.5 * self.delta      # field.py:237
+
+    @property
+    def composite(self) -> bool:
+        return len(self.nets) > 1 or self.scale != 1.0 or bool(np.any(self.centers != 0.0))
+
+    def predict(self, pos, ang):
+        """Distance and object id.  Single net: field.py:244-246 exactly."""
+        if not self.composite:
+            return net_predict(self.nets[0], pos, ang, self._ws[0]), np.zeros(len(pos), np.int32)
+        best = None
+        obj = np.zeros(len(pos), np.int32)
+        for j, net in enumerate(self.nets):
+            dj = self.scale * net_predict(net, (pos - self.centers[j]) / self.scale, ang, self._ws[j])
+            if best is None:
+                best = dj
+            else:
+                take = dj < best
+                obj[take] = j
+                best = np.where(take, dj, best)
+        return best, obj
+
+    def grad5(self, pos, ang, obj):
+        """field.py:291-293; composite: gradient of the object that was hit
+        (d/dx of s*f((x-c)/s) = grad f)."""
+        if not self.composite:
+            return net_grad5(self.nets[0], pos, ang, self._ws[0])
+        out = np.zeros((len(pos), 5))
+        for j, net in enumerate(self.nets):
+            sel = obj == j
+            if sel.any():
+                out[sel] = net_grad5(net, (pos[sel] - self.centers[j]) / self.scale, ang[sel], self._ws[j])
+        return out
+
+    # -- protocol ---------------------------------------------------------
+    def query(self, pos, dirs):
+        """field.py:248-258 query_batch: re-canonicalised angles, clamp,
+        hit = clamp < 0.98 delta, t = max(clamp, 0)."""
+        ang = dirs_to_angles(angles_to_dirs(dirs_to_angles(dirs)))
+        pred, _ = self.predict(np.atleast_2d(pos), ang)
+        c = np.clip(pred, -self.delta, self.delta)
+        return np.maximum(c, 0.0), c < HIT_FRACTION * self.delta
+
+    def trace(self, o, d, log=None):
+        """field.py:260-289 sphere march with per-step np.nonzero compaction.
+        Returns (t [inf on miss], hit, obj)."""
+        o = np.atleast_2d(np.asarray(o, dtype=np.float64))
+        d = np.atleast_2d(np.asarray(d, dtype=np.float64))
+        n = len(o)
+        ang = dirs_to_angles(d)
+        te, tx = ray_box(o, d, self.bounds[0], self.bounds[1])
+        alive = (te < tx) & (tx > 0.0)
+        tacc = np.where(alive, np.maximum(te, 0.0), 0.0)
+        tout = np.full(n, np.inf)
+        hit = np.zeros(n, dtype=bool)
+        obj = np.zeros(n, np.int32)
+        step = 0.9 * self.delta
+        thresh = HIT_FRACTION * self.delta
+        diag = float(np.linalg.norm(self.bounds[1] - self.bounds[0]))
+        for _ in range(int(np.ceil(diag / step)) + 4):
+            if not alive.any():
+                break
+            idx = np.nonzero(alive)[0]
+            if log is not None:
+                log.append(idx.copy())
+            p = o[idx] + tacc[idx, None] * d[idx]
+            pred, oid = self.predict(p, ang[idx])
+            c = np.clip(pred, -self.delta, self.delta)
+            found = c < thresh
+            sel = idx[found]
+            tout[sel] = tacc[sel] + np.maximum(c[found], 0.0)
+            hit[sel] = True
+            obj[sel] = oid[found]
+            alive[sel] = False
+            tacc[idx[~found]] += step
+            alive &= ~(alive & (tacc > tx))
+        return tout, hit, obj
+
+    def normal(self, o, d, t_hit=None, obj=None):
+        """field.py:295-317: gradient at max(t - delta/2, 0) along the ray,
+        normalised, flipped so n . d <= 0; |grad| < 1e-12 is invalid."""
+        o = np.atleast_2d(o)
+        d = np.atleast_2d(d)
+        if t_hit is not None:
+            back = np.maximum(np.asarray(t_hit) - self.normal_eval_backoff, 0.0)
+            p = o + back[:, None] * d
+        else:
+            p = o
+        if obj is None:
+            obj = np.zeros(len(o), np.int32)
+        g = self.grad5(p, dirs_to_angles(d), obj)[:, :3]
+        nrm = np.linalg.norm(g, axis=1)
+        valid = nrm >= 1e-12
+        n = np.zeros_like(g)
+        n[valid] = g[valid] / nrm[valid, None]
+        dots = np.einsum("ij,ij->i", n, d)
+        n[dots > 0.0] *= -1.0
+        return n, valid
+
+
+# --------------------------------------------------------------------------
+# camera and sampling (render.py:22-75, 127-141, 187-195; field.py:103-112)
+# --------------------------------------------------------------------------
+
+@dataclass
+class Cam:
+    """render.py:22-51 pinhole camera."""
+    position: np.ndarray
+    look_at: np.ndarray
+    up: np.ndarray = (0.0, 1.0, 0.0)
+    vfov: float = np.pi / 3.0
+    width: int = 256
+    height: int = 256
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=np.float64)
+        self.look_at = np.asarray(self.look_at, dtype=np.float64)
+        self.up = np.asarray(self.up, dtype=np.float64)
+        f = self.look_at - self.position
+        self.forward = f / np.linalg.norm(f)
+        r = np.cross(self.forward, self.up)
+        self.right = r / np.linalg.norm(r)
+        self.up_ortho = np.cross(self.right, self.forward)
+
+
+def camera_rays(cam: Cam, jitter, pix):
+    """render.py:54-75 restricted to the global pixel indices ``pix``."""
+    w, h = cam.width, cam.height
+    px = (pix % w).astype(np.float64)
+    py = (pix // w).astype(np.float64)
+    tan_half = np.tan(cam.vfov / 2.0)
+    aspect = w / h
+    sx = (2.0 * (px + jitter[:, 0]) / w - 1.0) * tan_half * aspect
+    sy = (1.0 - 2.0 * (py + jitter[:, 1]) / h) * tan_half
+    d = cam.forward[None, :] + sx[:, None] * cam.right[None, :] + sy[:, None] * cam.up_ortho[None, :]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return np.broadcast_to(cam.position, d.shape).copy(), d
+
+
+def frames(n):
+    """field.py:103-112 smallest-component orthonormal frames."""
+    axis = np.zeros((len(n), 3))
+    axis[np.arange(len(n)), np.argmin(np.abs(n), axis=1)] = 1.0
+    t1 = np.cross(n, axis)
+    t1 /= np.linalg.norm(t1, axis=1, keepdims=True)
+    return t1, np.cross(n, t1)
+
+
+def cosine_dirs(n, u):
+    """render.py:187-195 cosine-weighted hemisphere about n."""
+    r = np.sqrt(u[:, 0])
+    phi = 2.0 * np.pi * u[:, 1]
+    loc = np.stack([r * np.cos(phi), r * np.sin(phi), np.sqrt(np.maximum(0.0, 1.0 - u[:, 0]))], axis=1)
+    t1, t2 = frames(n)
+    return loc[:, 0, None] * t1 + loc[:, 1, None] * t2 + loc[:, 2, None] * n
+
+
+def hit_normals(fld: Field, o, d, t, obj):
+    """render.py:127-141 for an all-hit subset: degenerate -> -d, then the
+    n . d < 0 sign rule raises."""
+    n, valid = fld.normal(o, d, t_hit=t, obj=obj)
+    bad = ~valid
+    if bad.any():
+        n[bad] = -d[bad]
+    if not (np.einsum("ij,ij->i", n, d) < 0.0).all():
+        raise OracleNumericError("normal sign rule violated: n . dir >= 0")
+    return n
+
+
+# --------------------------------------------------------------------------
+# PCG64 (numpy's XSL-RR 128/64) as a counter-addressable stream
+# --------------------------------------------------------------------------
+
+def pcg_seed_state(seed: int, tag: int = RNG_TAG):
+    """(state, inc) of numpy default_rng([seed, tag]) (render.py:209)."""
+    st = np.random.PCG64(np.random.SeedSequence([seed, tag])).state["state"]
+    return int(st["state"]), int(st["inc"])
+
+
+def pcg_advance(state: int, inc: int, delta: int) -> int:
+    """LCG jump-ahead: state after ``delta`` steps (O(log delta))."""
+    am, ap, cm, cp = 1, 0, PCG_MULT, inc
+    while delta > 0:
+        if delta & 1:
+            am = (am * cm) & M128
+            ap = (ap * cm + cp) & M128
+        cp = ((cm + 1) * cp) & M128
+        cm = (cm * cm) & M128
+        delta >>= 1
+    return (am * state + ap) & M128
+
+
+def pcg_output(state: int) -> int:
+    """XSL-RR output of a post-step state."""
+    hi, lo = state >> 64, state & M64
+    x = hi ^ lo
+    r = hi >> 58
+    return ((x >> r) | (x << ((64 - r) & 63))) & M64
+
+
+def pcg_double(seed_state, k: int) -> float:
+    """Draw k (0-based) of the stream as numpy's Generator.random() makes it:
+    (next64 >> 11) * 2^-53, next64 taken after k+1 steps."""
+    s, inc = seed_state
+    return (pcg_output(pcg_advance(s, inc, k + 1)) >> 11) * (1.0 / 9007199254740992.0)
+
+
+def stream_block(seed: int, tag: int, k0: int, count: int):
+    """``count`` consecutive doubles from draw index k0 (numpy advance)."""
+    bg = np.random.PCG64(np.random.SeedSequence([seed, tag]))
+    if k0:
+        bg.advance(k0)
+    return np.random.Generator(bg).random(count)
+
+
+def draw_index(s: int, stage: int, n_pix: int, bounces: int) -> int:
+    """first draw of (sample s, stage j) where stage 0 is the
+    jitter and stage 1+b is bounce b; pixel i component c adds 2i + c."""
+    return (s * (bounces + 1) + stage) * 2 * n_pix
+
+
+# --------------------------------------------------------------------------
+# the path tracer (render.py:198-247)
+# --------------------------------------------------------------------------
+
+@dataclass
+class PathConfig:
+    spp: int = 16
+    bounces: int = 3
+    albedo: float = 0.7
+    env: float = 1.0
+    seed: int = 0
+    rr_start: int = -1          # EXTENSION: Russian roulette from this bounce index (-1 = off)
+
+
+def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None):
+    """render.py:198-247 over the contiguous global pixel range ``pix_range``
+    (default: the whole film).  Random draws are addressed by global index so
+    any range reproduces the full-frame stream.  Returns the (P,) grey value
+    per pixel of the range (accum / spp, film summed in spp order).
+
+    ``log`` (a list) receives, per spp, a dict with the ascending local
+    indices alive at each primary march step ("primary_march") and alive on
+    entry to each bounce ("bounce_alive"), for compaction parity.
+    EXTENSIONS: per-object albedo for composite fields; Russian roulette."""
+    if cfg.bounces < 1:
+        raise ValueError("path mode needs bounces >= 1")
+    n_pix = cam.width * cam.height
+    i0, i1 = (0, n_pix) if pix_range is None else pix_range
+    pix = np.arange(i0, i1)
+    P = len(pix)
+    accum = np.zeros(P)
+    alb = None if fld.albedos is None else np.asarray(fld.albedos, dtype=np.float64)
+    for s in range(cfg.spp):
+        jit = stream_block(cfg.seed, RNG_TAG, draw_index(s, 0, n_pix, cfg.bounces) + 2 * i0, 2 * P).reshape(P, 2)
+        o, d = camera_rays(cam, jit, pix)
+        rad = np.zeros(P)
+        thr = np.ones(P)
+        tl = [] if log is not None else None
+        t, hit, obj = fld.trace(o, d, tl)
+        rad[~hit] = cfg.env
+        alive = hit.copy()
+        pos = o
+        stages = []
+        for b in range(cfg.bounces):
+            u = stream_block(cfg.seed, RNG_TAG, draw_index(s, 1 + b, n_pix, cfg.bounces) + 2 * i0, 2 * P).reshape(P, 2)
+            if cfg.rr_start >= 0 and b >= cfg.rr_start and alive.any():
+                rr = stream_block(cfg.seed, RR_TAG, (s * cfg.bounces + b) * n_pix + i0, P)
+                idx = np.nonzero(alive)[0]
+                p = np.minimum(1.0, thr[idx])
+                live = rr[idx] < p
+                alive[idx[~live]] = False
+                thr[idx[live]] = thr[idx[live]] / p[live]
+            if not alive.any():
+                continue
+            idx = np.nonzero(alive)[0]
+            if log is not None:
+                stages.append(idx.copy())
+            nrm = hit_normals(fld, pos[idx], d[idx], t[idx], obj[idx])
+            hp = pos[idx] + t[idx, None] * d[idx] + 1e-6 * nrm
+            thr[idx] *= cfg.albedo if alb is None else alb[obj[idx]]
+            nd = cosine_dirs(nrm, u[idx])
+            tn, hn, on = fld.trace(hp, nd)
+            esc = idx[~hn]
+            rad[esc] += thr[esc] * cfg.env
+            alive[esc] = False
+            cont = idx[hn]
+            pos[cont] = hp[hn]
+            d[cont] = nd[hn]
+            t[cont] = tn[hn]
+            obj[cont] = on[hn]
+            nxt = np.zeros(P, dtype=bool)
+            nxt[cont] = True
+            alive = nxt
+        accum += rad
+        if log is not None:
+            log.append({"primary_march": tl, "bounce_alive": stages})
+    return accum / cfg.spp
+
+
+def film_rgb(value, cam: Cam):
+    """render.py:244-247 grey -> (H, W, 3)."""
+    return np.repeat(value[:, None], 3, axis=1).reshape(cam.height, cam.width, 3)
