@@ -1,0 +1,128 @@
+/* C ABI of the B200 DDF hot path (libddf_b200.so).
+ *
+ * The reference (ddfield, pure Python) has no FFI; its "plugin interface" for
+ * this path is the duck-typed backend protocol that render.render_* calls
+ * (ddfield/field.py:161-186, 248-317, 320) plus render.render_path
+ * (ddfield/render.py:198-247) and the DDFN weight layout
+ * (ddfield/neural.py:378-431).  Each entry point below replaces one of those
+ * and cites it.  The Python shim paper_2306_16142_b200.field.CudaNeuralField
+ * binds them with ctypes.
+ *
+ * Conventions
+ *  - Array arguments are DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ *    C-contiguous, float64 unless stated; (N,3) arrays are row-major xyz.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    stream-ordered; ddf_render_path synchronises the stream before returning
+ *    because it reports numeric errors.
+ *  - One call at a time per field handle (its scratch is reused); handles are
+ *    independent, so concurrent calls on different handles are fine.
+ *  - Return value: DDF_OK or an error class mirroring ddfield/errors.py;
+ *    ddf_last_error() holds the message (thread-local).
+ */
+#ifndef DDF_B200_H
+#define DDF_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDF_OK 0
+#define DDF_EUSAGE 1   /* ValueError / usage (cli.py:502-517 exit 1)       */
+#define DDF_EDATA 2    /* DataError   (errors.py:12-13, exit 2)             */
+#define DDF_ENUMERIC 3 /* NumericError (errors.py:16-17, exit 3)            */
+#define DDF_ECUDA 4    /* CUDA runtime failure                             */
+
+#define DDF_PREC_FP32 0 /* exact fp32 FFMA MLP                            */
+#define DDF_PREC_BF16 1 /* tcgen05 bf16 MLP, fp32 accumulate              */
+
+#define DDF_ENC_RAW5 0  /* neural.py:26-38 (x,y,z,az/pi-1,2pol/pi-1)      */
+#define DDF_ENC_PE6 1   /* + 6-octave sin/cos encoding -> 65 inputs (configs 3-5) */
+
+typedef struct ddf_field_s* ddf_field_t;
+
+typedef struct {
+  /* render.Camera after __post_init__ (render.py:33-51), computed by the host */
+  double position[3], forward[3], right[3], up_ortho[3];
+  double tan_half; /* tan(vfov/2) */
+  double aspect;   /* width/height */
+  int32_t width, height;
+} ddf_camera_t;
+
+typedef struct {
+  /* render.RenderConfig fields used by render_path (render.py:106-124) */
+  int32_t spp, bounces;
+  double albedo, env_radiance;
+  /* numpy PCG64 of default_rng([seed, 0x9A7]) (render.py:209): 128-bit state
+     and increment as (lo, hi) u64 pairs, from bit_generator.state */
+  uint64_t rng_state[2], rng_inc[2];
+  /* EXTENSION (config 4): Russian roulette from this bounce index, -1 = off,
+     with its own PCG64 stream */
+  int32_t rr_start;
+  uint64_t rr_state[2], rr_inc[2];
+  /* image-tile sharding (config 4): tiles of tile x tile pixels, row-major,
+     tile k owned by rank k % world; tile = 0 renders every pixel */
+  int32_t tile, rank, world;
+  /* path slots per wave (0 = default); larger waves mean fewer launches */
+  int64_t max_wave_paths;
+} ddf_path_config_t;
+
+typedef struct {
+  uint64_t forward_rows;   /* MLP forward rows evaluated (DDF queries)       */
+  uint64_t gradient_rows;  /* MLP input-gradient rows (normals)             */
+  uint64_t degenerate;     /* normals that fell back to -d (render.py:133)  */
+  uint64_t path_samples;   /* owned pixels x spp                            */
+  int32_t waves;
+} ddf_render_stats_t;
+
+/* NeuralField.__init__ (field.py:231-237): delta, AABB bounds (lo xyz, hi xyz). */
+int ddf_field_create(double delta, const double bounds[6], int32_t precision, int32_t device,
+                     ddf_field_t* out);
+/* Adds one network.  MlpModel (neural.py:41-74) after effective_weights():
+   `weights` = concatenation over layers of W_l (out, in) row-major float64,
+   `biases` = concatenation of b_l.  HOST pointers.  center/scale/albedo are
+   the EXTENSION object transform of config 5 (0, 1, unused for one net). */
+int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths, const double* weights,
+                          const double* biases, int32_t encoding, const double center[3], double scale,
+                          double albedo);
+int ddf_field_destroy(ddf_field_t f);
+/* Switch the MLP engine of an existing field (DDF_PREC_*). */
+int ddf_field_set_precision(ddf_field_t f, int32_t precision);
+const char* ddf_last_error(void);
+
+/* neural.forward_batch (neural.py:138-157) of network `net` on raw inputs
+   x (n, widths[0]) -> out (n,) */
+int ddf_mlp_forward(ddf_field_t f, int32_t net, const double* x, int64_t n, double* out, void* stream);
+/* neural.input_gradient_batch (neural.py:229-249) -> out (n, widths[0]) */
+int ddf_mlp_input_grad(ddf_field_t f, int32_t net, const double* x, int64_t n, double* out, void* stream);
+/* NeuralField.query_batch (field.py:248-258): t (n,), hit (n,) uint8;
+   pred (nullable) receives the raw network distance (config 1's output),
+   obj (nullable) the min-composite object id */
+int ddf_query(ddf_field_t f, const double* pos, const double* dirs, int64_t n, double* t, uint8_t* hit,
+              double* pred, int32_t* obj, void* stream);
+/* NeuralField.trace_batch (field.py:260-289): t (inf on miss), hit, obj (nullable) */
+int ddf_trace(ddf_field_t f, const double* origins, const double* dirs, int64_t n, double* t, uint8_t* hit,
+              int32_t* obj, void* stream);
+/* NeuralField.normal_batch (field.py:295-317): t_hit and obj nullable;
+   normals (n,3), valid (n,) uint8 */
+int ddf_normal(ddf_field_t f, const double* origins, const double* dirs, const double* t_hit, const int32_t* obj,
+               int64_t n, double* normals, uint8_t* valid, void* stream);
+/* render.render_path (render.py:198-247): adds each owned pixel's radiance
+   summed over spp (in sample order) into accum (W*H,) -- the caller divides
+   by spp and replicates grey to RGB (render.py:244-247).  accum is zeroed
+   first.  DDF_ENUMERIC on the normal sign rule (render.py:137-139). */
+int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_config_t* cfg, double* accum,
+                    ddf_render_stats_t* stats, void* stream);
+
+/* np.random.default_rng(...).random() draw k of a PCG64 stream given its
+   (state, inc) (render.py:209,213,222): out[j] = draw idx[j] (device arrays). */
+int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64_t* idx, int64_t n, double* out,
+                    void* stream);
+/* np.nonzero(flags) (field.py:277, render.py:225): ascending indices of the
+   non-zero uint8 flags into list (device), count written to *count (device int32). */
+int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

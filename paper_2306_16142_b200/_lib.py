@@ -1,0 +1,124 @@
+"""ctypes binding of libddf_b200.so (include/ddf_b200.h) and its build recipe.
+
+The library is built in-tree (``paper_2306_16142_b200/lib/libddf_b200.so``)
+with nvcc for sm_100a only.  There is no CPU fallback: every entry point of the
+package fails loudly when the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+from .errors import DataError, DdfError, NumericError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB_DIR = os.path.join(HERE, "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libddf_b200.so")
+HEADER = os.path.join(ROOT, "include", "ddf_b200.h")
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+
+DDF_OK, DDF_EUSAGE, DDF_EDATA, DDF_ENUMERIC, DDF_ECUDA = 0, 1, 2, 3, 4
+PREC_FP32, PREC_BF16 = 0, 1
+ENC_RAW5, ENC_PE6 = 0, 1
+
+EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "ddf_field_set_precision",
+           "ddf_last_error", "ddf_mlp_forward", "ddf_mlp_input_grad", "ddf_query", "ddf_trace",
+           "ddf_normal", "ddf_render_path", "ddf_rng_doubles", "ddf_compact")
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile the CUDA sources into the in-tree shared library."""
+    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))]
+    if not force and os.path.exists(LIB_PATH):
+        newest = max(os.path.getmtime(p) for p in srcs + [HEADER])
+        if os.path.getmtime(LIB_PATH) >= newest:
+            return LIB_PATH
+    os.makedirs(LIB_DIR, exist_ok=True)
+    nvcc = os.environ.get("NVCC", "nvcc")
+    tmp = LIB_PATH + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, os.path.join(CSRC, "ddf_api.cu"), "-o", tmp]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    if verbose:
+        print(res.stdout + res.stderr)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class Camera_t(ctypes.Structure):
+    _fields_ = [("position", ctypes.c_double * 3), ("forward", ctypes.c_double * 3),
+                ("right", ctypes.c_double * 3), ("up_ortho", ctypes.c_double * 3),
+                ("tan_half", ctypes.c_double), ("aspect", ctypes.c_double),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class PathConfig_t(ctypes.Structure):
+    _fields_ = [("spp", ctypes.c_int32), ("bounces", ctypes.c_int32),
+                ("albedo", ctypes.c_double), ("env_radiance", ctypes.c_double),
+                ("rng_state", ctypes.c_uint64 * 2), ("rng_inc", ctypes.c_uint64 * 2),
+                ("rr_start", ctypes.c_int32),
+                ("rr_state", ctypes.c_uint64 * 2), ("rr_inc", ctypes.c_uint64 * 2),
+                ("tile", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("max_wave_paths", ctypes.c_int64)]
+
+
+class RenderStats_t(ctypes.Structure):
+    _fields_ = [("forward_rows", ctypes.c_uint64), ("gradient_rows", ctypes.c_uint64),
+                ("degenerate", ctypes.c_uint64), ("path_samples", ctypes.c_uint64),
+                ("waves", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load (building first if needed and possible) the shared library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        build()
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    L.ddf_last_error.restype = ctypes.c_char_p
+    L.ddf_field_create.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_double), i32, i32, ctypes.POINTER(vp)]
+    L.ddf_field_add_network.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), i32, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.c_double, ctypes.c_double]
+    L.ddf_field_destroy.argtypes = [vp]
+    L.ddf_field_set_precision.argtypes = [vp, i32]
+    L.ddf_mlp_forward.argtypes = [vp, i32, dp, i64, dp, vp]
+    L.ddf_mlp_input_grad.argtypes = [vp, i32, dp, i64, dp, vp]
+    L.ddf_query.argtypes = [vp, dp, dp, i64, dp, dp, dp, dp, vp]
+    L.ddf_trace.argtypes = [vp, dp, dp, i64, dp, dp, dp, vp]
+    L.ddf_normal.argtypes = [vp, dp, dp, dp, dp, i64, dp, dp, vp]
+    L.ddf_render_path.argtypes = [vp, ctypes.POINTER(Camera_t), ctypes.POINTER(PathConfig_t), dp,
+                                  ctypes.POINTER(RenderStats_t), vp]
+    L.ddf_rng_doubles.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64), dp, i64, dp, vp]
+    L.ddf_compact.argtypes = [dp, i64, dp, dp, vp]
+    for name in EXPORTS:
+        if name != "ddf_last_error":
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    """Map a C status onto the reference's exception classes (errors.py:8-17)."""
+    if rc == DDF_OK:
+        return
+    msg = lib().ddf_last_error().decode("utf-8", "replace")
+    if rc == DDF_EUSAGE:
+        raise ValueError(msg)
+    if rc == DDF_EDATA:
+        raise DataError(msg)
+    if rc == DDF_ENUMERIC:
+        raise NumericError(msg)
+    raise DdfError(f"CUDA failure: {msg}")

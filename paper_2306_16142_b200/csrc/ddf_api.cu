@@ -1,0 +1,605 @@
+// libddf_b200.so: the C ABI (include/ddf_b200.h) over the sm_100a kernels.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ddf_b200.h"
+#include "compact.cuh"
+#include "ddf_common.cuh"
+#include "field_kernels.cuh"
+#include "mlp_umma.cuh"
+#include "wavefront.cuh"
+
+using namespace ddf;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) return fail(DDF_ECUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+int pad16(int w) { return (w + 15) / 16 * 16; }
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct ddf_field_s {
+  FieldDev F{};                 // host copy holding device pointers
+  FieldDev* F_dev = nullptr;    // device copy (BounceOp reads albedos through it)
+  std::vector<void*> weights;   // device weight allocations
+  std::vector<umma::NetImage> images;
+  int device = 0;
+  int sm_count = 148;
+  // scratch
+  Buf t_acc, t_exit, alive, list, list2, blocks, small, ones;
+  Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
+  Buf pix, rng;
+  int pix_key[6] = {-1, -1, -1, -1, -1, -1};
+  int pix_n = 0;
+};
+
+namespace {
+
+// small scratch layout: [0..15] seg, [16] count, [17] count2, [18..19] err, u64 stats after 32 ints
+struct Small {
+  int* seg; int* count; int* count2; int* err; unsigned long long* stats;  // stats[0]=fwd [1]=grad [2]=degenerate
+};
+Small small_of(ddf_field_s* f) {
+  Small s;
+  int* b = f->small.as<int>();
+  s.seg = b;
+  s.count = b + 16;
+  s.count2 = b + 17;
+  s.err = b + 18;
+  s.stats = reinterpret_cast<unsigned long long*>(b + 32);
+  return s;
+}
+
+int max_width(const FieldDev& F) {
+  int w = 0;
+  for (int j = 0; j < F.n_obj; ++j)
+    for (int l = 0; l <= F.net[j].n_layers; ++l) w = std::max(w, F.net[j].widths[l]);
+  return w;
+}
+
+// ---------------------------------------------------------------- engine dispatch
+template <int M, int KMAX>
+size_t simt_smem() {
+  return sizeof(double) * M * 8 + sizeof(float) * (2 * KMAX * M + simt::KC * simt::NC + 2 * M) +
+         sizeof(uint32_t) * DDF_MAX_LAYERS * KMAX * (M / 32) + sizeof(int) * 2 * M;
+}
+
+template <class Op, int M, int KMAX>
+int launch_simt(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool grad, cudaStream_t st) {
+  const size_t sm = simt_smem<M, KMAX>();
+  void (*kern)(const FieldDev, const Op);
+  if constexpr (Op::kGrad) kern = simt::grad_kernel<M, KMAX, Op>;
+  else kern = simt::forward_kernel<M, KMAX, Op>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int tiles = (max_rows + M - 1) / M + (grad ? F.n_obj : 0);
+  int grid = std::max(1, std::min(tiles, f->sm_count));
+  kern<<<grid, simt::NT, sm, st>>>(F, op);
+  CUDA_TRY(cudaGetLastError());
+  return DDF_OK;
+}
+
+template <class Op>
+int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool grad, cudaStream_t st) {
+  if (max_rows <= 0) return DDF_OK;
+  if (F.precision == PREC_BF16) return umma::launch<Op>(F, op, max_rows, grad, f->sm_count, st, &g_err);
+  const int w = max_width(F);
+  if (w <= 256) return launch_simt<Op, 64, 256>(f, F, op, max_rows, grad, st);
+  if (w <= 512) return launch_simt<Op, 32, 512>(f, F, op, max_rows, grad, st);
+  return fail(DDF_EUSAGE, "fp32 engine supports layer widths up to 512");
+}
+
+// stable compaction flags -> list (+ segments by object when obj != nullptr)
+int compact_flags(ddf_field_s* f, const uint8_t* flags, const int* obj, int n, int n_obj, int* list, int* seg,
+                  int* count, unsigned long long* rows_acc, cudaStream_t st) {
+  const int nb = std::max(1, (n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS);
+  CUDA_TRY(f->blocks.ensure(sizeof(int) * nb * DDF_MAX_OBJECTS));
+  int* bc = f->blocks.as<int>();
+  const int no = obj ? n_obj : 1;
+  compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, obj, n, no, bc);
+  compact::scan_kernel<<<1, 1024, 0, st>>>(bc, nb, no, seg, count, rows_acc);
+  compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, obj, n, no, bc, list);
+  CUDA_TRY(cudaGetLastError());
+  return DDF_OK;
+}
+
+__global__ void trace_init_kernel(const FieldDev F, MarchState S, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const d3 o = ld3(S.o, i), d = ld3(S.d, i);
+  double te, tx;
+  ray_box(o, d, F.lo, F.hi, te, tx);
+  const bool in = (te < tx) && (tx > 0.0);
+  S.t_acc[i] = in ? fmax(te, 0.0) : 0.0;
+  const_cast<double*>(S.t_exit)[i] = tx;
+  S.alive[i] = in;
+  S.t_out[i] = INFINITY;
+  S.hit[i] = 0;
+  if (S.obj) S.obj[i] = 0;
+}
+
+// sphere march over the slots whose `march` flag is set (field.py:274-288)
+int march(ddf_field_s* f, const MarchState& ms, int n, int* list, unsigned long long* fwd_acc, cudaStream_t st) {
+  Small sm = small_of(f);
+  for (int step = 0; step < f->F.max_steps; ++step) {
+    int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st);
+    if (rc) return rc;
+    TraceStepOp op{};
+    op.list = list; op.count = sm.count; op.n = n; op.seg = nullptr;
+    op.st = ms; op.delta = f->F.delta; op.thresh = f->F.thresh; op.step = f->F.step;
+    rc = run_mlp(f, f->F, op, n, false, st);
+    if (rc) return rc;
+  }
+  return DDF_OK;
+}
+
+void build_stream(const uint64_t st[2], const uint64_t inc[2], PcgStream* out) {
+  typedef unsigned __int128 U;
+  const U mult = ((U)0x2360ED051FC65DA4ull << 64) | (U)0x4385DF649FCCF645ull;
+  U cm = mult, cp = ((U)inc[1] << 64) | inc[0];
+  out->state = u128{st[0], st[1]};
+  for (int b = 0; b < 64; ++b) {
+    out->mult[b] = u128{(uint64_t)cm, (uint64_t)(cm >> 64)};
+    out->plus[b] = u128{(uint64_t)cp, (uint64_t)(cp >> 64)};
+    cp = (cm + 1) * cp;
+    cm = cm * cm;
+  }
+}
+
+int ensure_small(ddf_field_s* f) {
+  CUDA_TRY(f->small.ensure(4096));
+  return DDF_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* ddf_last_error(void) { return g_err.c_str(); }
+
+int ddf_field_create(double delta, const double bounds[6], int32_t precision, int32_t device, ddf_field_t* out) {
+  if (!out) return fail(DDF_EUSAGE, "null output handle");
+  if (!(delta > 0.0)) return fail(DDF_EUSAGE, "delta must be positive");
+  if (precision != DDF_PREC_FP32 && precision != DDF_PREC_BF16) return fail(DDF_EUSAGE, "unknown precision");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(DDF_ECUDA, "no CUDA device: the B200 DDF path has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(DDF_EUSAGE, "bad device index");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(DDF_ECUDA, "libddf_b200 is built for sm_100a (B200) only");
+  auto* f = new ddf_field_s();
+  f->device = device;
+  f->sm_count = prop.multiProcessorCount;
+  FieldDev& F = f->F;
+  F.n_obj = 0;
+  F.precision = precision;
+  F.delta = delta;
+  for (int k = 0; k < 3; ++k) { F.lo[k] = bounds[k]; F.hi[k] = bounds[3 + k]; }
+  F.step = 0.9 * delta;
+  F.thresh = DDF_HIT_FRACTION * delta;
+  F.backoff = 0.5 * delta;
+  const double dx = bounds[3] - bounds[0], dy = bounds[4] - bounds[1], dz = bounds[5] - bounds[2];
+  const double diag = std::sqrt((dx * dx + dy * dy) + dz * dz);
+  F.max_steps = (int)std::ceil(diag / F.step) + 4;
+  F.composite = false;
+  if (cudaMalloc(&f->F_dev, sizeof(FieldDev)) != cudaSuccess) {
+    delete f;
+    return fail(DDF_ECUDA, "cudaMalloc failed");
+  }
+  *out = f;
+  return DDF_OK;
+}
+
+int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths, const double* weights,
+                          const double* biases, int32_t encoding, const double center[3], double scale,
+                          double albedo) {
+  if (!f || !widths || !weights || !biases) return fail(DDF_EUSAGE, "null argument");
+  if (f->F.n_obj >= DDF_MAX_OBJECTS) return fail(DDF_EUSAGE, "too many networks in one field");
+  const int L = n_widths - 1;
+  if (L < 1 || L > DDF_MAX_LAYERS) return fail(DDF_EUSAGE, "unsupported layer count");
+  if (widths[L] != 1) return fail(DDF_EDATA, "network head must have width 1");
+  for (int l = 0; l < n_widths; ++l)
+    if (widths[l] < 1) return fail(DDF_EDATA, "bad layer width");
+  if (encoding == DDF_ENC_RAW5 && widths[0] != 5) return fail(DDF_EDATA, "raw encoding needs 5 inputs");
+  if (encoding == DDF_ENC_PE6 && widths[0] != 65) return fail(DDF_EDATA, "PE encoding needs 65 inputs");
+  if (!(scale > 0.0)) return fail(DDF_EUSAGE, "scale must be positive");
+  CUDA_TRY(cudaSetDevice(f->device));
+  NetDev& N = f->F.net[f->F.n_obj];
+  N = NetDev{};
+  N.n_layers = L;
+  N.encoding = encoding;
+  for (int k = 0; k < 3; ++k) N.center[k] = center ? center[k] : 0.0;
+  N.scale = scale;
+  N.albedo = albedo;
+  std::vector<int> wp(L + 1);
+  for (int l = 0; l < L; ++l) wp[l] = pad16(widths[l]);
+  wp[L] = 1;
+  for (int l = 0; l <= L; ++l) N.widths[l] = wp[l];
+  N.max_width = *std::max_element(wp.begin(), wp.end());
+  size_t woff = 0, boff = 0;
+  for (int l = 0; l < L; ++l) {
+    const int in = widths[l], out = widths[l + 1], pin = wp[l], pout = wp[l + 1];
+    std::vector<float> w((size_t)pout * pin, 0.f), wt((size_t)pin * pout, 0.f), b(pout, 0.f);
+    for (int o = 0; o < out; ++o) {
+      for (int i = 0; i < in; ++i) {
+        const float v = (float)weights[woff + (size_t)o * in + i];
+        w[(size_t)o * pin + i] = v;
+        wt[(size_t)i * pout + o] = v;
+      }
+      b[o] = (float)biases[boff + o];
+    }
+    woff += (size_t)out * in;
+    boff += out;
+    float *dw, *dwt, *db;
+    CUDA_TRY(cudaMalloc(&dw, w.size() * 4));
+    CUDA_TRY(cudaMalloc(&dwt, wt.size() * 4));
+    CUDA_TRY(cudaMalloc(&db, std::max<size_t>(16, b.size() * 4)));
+    CUDA_TRY(cudaMemcpy(dw, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dwt, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(db, b.data(), b.size() * 4, cudaMemcpyHostToDevice));
+    f->weights.push_back(dw);
+    f->weights.push_back(dwt);
+    f->weights.push_back(db);
+    N.w[l] = dw;
+    N.wt[l] = dwt;
+    N.b[l] = db;
+  }
+  // bf16 UMMA weight images (built for every net; used when precision == BF16)
+  umma::NetImage img;
+  int rc = umma::build_image(widths, n_widths, weights, biases, &img, &g_err);
+  if (rc) return rc;
+  f->images.push_back(img);
+  N.wimg_fwd = img.dev;
+  N.wimg_bwd = img.dev;
+  f->F.n_obj += 1;
+  // composite as soon as there is more than one object or a transform
+  bool comp = f->F.n_obj > 1;
+  for (int j = 0; j < f->F.n_obj; ++j) {
+    const NetDev& n = f->F.net[j];
+    if (n.scale != 1.0 || n.center[0] != 0.0 || n.center[1] != 0.0 || n.center[2] != 0.0) comp = true;
+  }
+  f->F.composite = comp;
+  CUDA_TRY(cudaMemcpy(f->F_dev, &f->F, sizeof(FieldDev), cudaMemcpyHostToDevice));
+  return DDF_OK;
+}
+
+int ddf_field_set_precision(ddf_field_t f, int32_t precision) {
+  if (!f) return fail(DDF_EUSAGE, "null field");
+  if (precision != DDF_PREC_FP32 && precision != DDF_PREC_BF16) return fail(DDF_EUSAGE, "unknown precision");
+  f->F.precision = precision;
+  CUDA_TRY(cudaSetDevice(f->device));
+  CUDA_TRY(cudaMemcpy(f->F_dev, &f->F, sizeof(FieldDev), cudaMemcpyHostToDevice));
+  return DDF_OK;
+}
+
+int ddf_field_destroy(ddf_field_t f) {
+  if (!f) return DDF_OK;
+  cudaSetDevice(f->device);
+  for (void* p : f->weights) cudaFree(p);
+  for (auto& im : f->images) umma::free_image(&im);
+  Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones,
+                 &f->st_o, &f->st_d, &f->st_tacc, &f->st_texit, &f->st_t, &f->st_thr, &f->st_rad,
+                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng};
+  for (Buf* b : bufs) b->release();
+  if (f->F_dev) cudaFree(f->F_dev);
+  delete f;
+  return DDF_OK;
+}
+
+static int check_net(ddf_field_t f, int net) {
+  if (!f) return fail(DDF_EUSAGE, "null field");
+  if (net < 0 || net >= f->F.n_obj) return fail(DDF_EUSAGE, "bad network index");
+  return DDF_OK;
+}
+
+static FieldDev single_net(const FieldDev& F, int net) {
+  FieldDev G = F;
+  G.n_obj = 1;
+  G.composite = false;
+  G.net[0] = F.net[net];
+  return G;
+}
+
+int ddf_mlp_forward(ddf_field_t f, int32_t net, const double* x, int64_t n, double* out, void* stream) {
+  if (int rc = check_net(f, net)) return rc;
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
+  if (n == 0) return DDF_OK;
+  CUDA_TRY(cudaSetDevice(f->device));
+  RawForwardOp op{};
+  op.list = nullptr; op.count = nullptr; op.n = (int)n; op.seg = nullptr;
+  op.x = x; op.width = f->images[net].in_width; op.out = out;   // unpadded row stride
+  return run_mlp(f, single_net(f->F, net), op, (int)n, false, (cudaStream_t)stream);
+}
+
+int ddf_mlp_input_grad(ddf_field_t f, int32_t net, const double* x, int64_t n, double* out, void* stream) {
+  if (int rc = check_net(f, net)) return rc;
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
+  if (n == 0) return DDF_OK;
+  CUDA_TRY(cudaSetDevice(f->device));
+  RawGradOp op{};
+  op.list = nullptr; op.count = nullptr; op.n = (int)n; op.seg = nullptr;
+  op.x = x; op.width = f->images[net].in_width; op.out = out;
+  return run_mlp(f, single_net(f->F, net), op, (int)n, true, (cudaStream_t)stream);
+}
+
+int ddf_query(ddf_field_t f, const double* pos, const double* dirs, int64_t n, double* t, uint8_t* hit,
+              double* pred, int32_t* obj, void* stream) {
+  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
+  if (n == 0) return DDF_OK;
+  CUDA_TRY(cudaSetDevice(f->device));
+  QueryOp op{};
+  op.list = nullptr; op.count = nullptr; op.n = (int)n; op.seg = nullptr;
+  op.pos = pos; op.dirs = dirs; op.t = t; op.hit = hit; op.pred_out = pred; op.obj_out = obj;
+  op.delta = f->F.delta; op.thresh = f->F.thresh;
+  return run_mlp(f, f->F, op, (int)n, false, (cudaStream_t)stream);
+}
+
+int ddf_trace(ddf_field_t f, const double* origins, const double* dirs, int64_t n, double* t, uint8_t* hit,
+              int32_t* obj, void* stream) {
+  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
+  if (n == 0) return DDF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(f->device));
+  if (int rc = ensure_small(f)) return rc;
+  CUDA_TRY(f->t_acc.ensure(sizeof(double) * n));
+  CUDA_TRY(f->t_exit.ensure(sizeof(double) * n));
+  CUDA_TRY(f->alive.ensure(n));
+  CUDA_TRY(f->list.ensure(sizeof(int) * n));
+  CUDA_TRY(f->st_obj.ensure(sizeof(int) * n));
+  MarchState ms{};
+  ms.o = origins; ms.d = dirs;
+  ms.t_acc = f->t_acc.as<double>(); ms.t_exit = f->t_exit.as<double>();
+  ms.alive = f->alive.as<uint8_t>(); ms.t_out = t; ms.hit = hit;
+  ms.obj = obj ? obj : f->st_obj.as<int>();
+  trace_init_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(f->F, ms, (int)n);
+  CUDA_TRY(cudaGetLastError());
+  return march(f, ms, (int)n, f->list.as<int>(), nullptr, st);
+}
+
+int ddf_normal(ddf_field_t f, const double* origins, const double* dirs, const double* t_hit, const int32_t* obj,
+               int64_t n, double* normals, uint8_t* valid, void* stream) {
+  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
+  if (n == 0) return DDF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(f->device));
+  if (int rc = ensure_small(f)) return rc;
+  NormalOp op{};
+  op.o = origins; op.d = dirs; op.t_hit = t_hit; op.backoff = f->F.backoff; op.normals = normals; op.valid = valid;
+  op.n = (int)n; op.count = nullptr; op.list = nullptr; op.seg = nullptr;
+  if (f->F.n_obj > 1) {
+    if (!obj) return fail(DDF_EUSAGE, "composite fields need the hit object ids for normals");
+    CUDA_TRY(f->ones.ensure(n));
+    CUDA_TRY(cudaMemsetAsync(f->ones.p, 1, n, st));
+    CUDA_TRY(f->list.ensure(sizeof(int) * n));
+    Small sm = small_of(f);
+    if (int rc = compact_flags(f, f->ones.as<uint8_t>(), obj, (int)n, f->F.n_obj, f->list.as<int>(), sm.seg,
+                               sm.count, nullptr, st))
+      return rc;
+    op.list = f->list.as<int>(); op.count = sm.count; op.seg = sm.seg;
+  }
+  return run_mlp(f, f->F, op, (int)n, true, st);
+}
+
+int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_config_t* cfg, double* accum,
+                    ddf_render_stats_t* stats, void* stream) {
+  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (!cam || !cfg || !accum) return fail(DDF_EUSAGE, "null argument");
+  if (cfg->bounces < 1) return fail(DDF_EUSAGE, "path mode needs bounces >= 1");   // render.py:207-208
+  if (cfg->spp < 1) return fail(DDF_EUSAGE, "spp must be >= 1");                 // render.py:119-120
+  if (cam->width < 1 || cam->height < 1) return fail(DDF_EUSAGE, "film dimensions must be >= 1");
+  const int64_t n_pix = (int64_t)cam->width * cam->height;
+  if (n_pix > (1ll << 30)) return fail(DDF_EUSAGE, "film too large");
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world || cfg->tile < 0)
+    return fail(DDF_EUSAGE, "bad tile sharding");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(f->device));
+  if (int rc = ensure_small(f)) return rc;
+  Small sm = small_of(f);
+
+  // owned pixels, ascending global index (cached per film/sharding)
+  const int key[6] = {cam->width, cam->height, cfg->tile, cfg->rank, cfg->world, 1};
+  if (std::memcmp(key, f->pix_key, sizeof(key)) != 0) {
+    std::vector<int> own;
+    own.reserve(n_pix / cfg->world + 1);
+    const int T = cfg->tile;
+    const int ntx = T > 0 ? (cam->width + T - 1) / T : 1;
+    for (int64_t i = 0; i < n_pix; ++i) {
+      if (T > 0) {
+        const int px = (int)(i % cam->width), py = (int)(i / cam->width);
+        const int tile_id = (py / T) * ntx + px / T;
+        if (tile_id % cfg->world != cfg->rank) continue;
+      } else if (cfg->world > 1 && (i % cfg->world) != cfg->rank) {
+        continue;
+      }
+      own.push_back((int)i);
+    }
+    CUDA_TRY(f->pix.ensure(sizeof(int) * std::max<size_t>(1, own.size())));
+    if (!own.empty())
+      CUDA_TRY(cudaMemcpy(f->pix.p, own.data(), sizeof(int) * own.size(), cudaMemcpyHostToDevice));
+    std::memcpy(f->pix_key, key, sizeof(key));
+    f->pix_n = (int)own.size();
+  }
+  const int n_own = f->pix_n;
+  CUDA_TRY(cudaMemsetAsync(accum, 0, sizeof(double) * n_pix, st));
+  CUDA_TRY(cudaMemsetAsync(f->small.p, 0, 4096, st));
+  if (n_own == 0) {
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return DDF_OK;
+  }
+
+  // RNG jump tables
+  PcgStream hs[2];
+  build_stream(cfg->rng_state, cfg->rng_inc, &hs[0]);
+  build_stream(cfg->rr_state, cfg->rr_inc, &hs[1]);
+  CUDA_TRY(f->rng.ensure(sizeof(hs)));
+  CUDA_TRY(cudaMemcpyAsync(f->rng.p, hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+
+  // wave sizing
+  int64_t maxp = cfg->max_wave_paths > 0 ? cfg->max_wave_paths : (int64_t)8 << 20;
+  int ns = (int)std::max<int64_t>(1, std::min<int64_t>(cfg->spp, maxp / n_own));
+  const int64_t P64 = (int64_t)ns * n_own;
+  if (P64 > (1ll << 30)) return fail(DDF_EUSAGE, "wave too large");
+  const int P = (int)P64;
+  CUDA_TRY(f->st_o.ensure(sizeof(double) * 3 * P));
+  CUDA_TRY(f->st_d.ensure(sizeof(double) * 3 * P));
+  CUDA_TRY(f->st_tacc.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_texit.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_t.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_thr.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_rad.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_hit.ensure(P));
+  CUDA_TRY(f->st_march.ensure(P));
+  CUDA_TRY(f->st_alive.ensure(P));
+  CUDA_TRY(f->st_obj.ensure(sizeof(int) * P));
+  CUDA_TRY(f->list.ensure(sizeof(int) * P));
+  CUDA_TRY(f->list2.ensure(sizeof(int) * P));
+
+  PathState S{};
+  S.o = f->st_o.as<double>(); S.d = f->st_d.as<double>();
+  S.t_acc = f->st_tacc.as<double>(); S.t_exit = f->st_texit.as<double>(); S.t = f->st_t.as<double>();
+  S.thr = f->st_thr.as<double>(); S.rad = f->st_rad.as<double>();
+  S.hit = f->st_hit.as<uint8_t>(); S.march = f->st_march.as<uint8_t>(); S.alive = f->st_alive.as<uint8_t>();
+  S.obj = f->st_obj.as<int>();
+  MarchState ms{};
+  ms.o = S.o; ms.d = S.d; ms.t_acc = S.t_acc; ms.t_exit = S.t_exit; ms.alive = S.march;
+  ms.t_out = S.t; ms.hit = S.hit; ms.obj = S.obj;
+
+  CamDev C{};
+  for (int k = 0; k < 3; ++k) {
+    C.pos[k] = cam->position[k]; C.fwd[k] = cam->forward[k]; C.right[k] = cam->right[k]; C.up[k] = cam->up_ortho[k];
+  }
+  C.tan_half = cam->tan_half; C.aspect = cam->aspect; C.W = cam->width; C.H = cam->height;
+
+  WaveDev w{};
+  w.spp = cfg->spp; w.bounces = cfg->bounces; w.albedo = cfg->albedo; w.env = cfg->env_radiance;
+  w.rr_start = cfg->rr_start; w.n_pix = n_pix; w.pix = f->pix.as<int>(); w.n_own = n_own;
+  w.rng = f->rng.as<PcgStream>(); w.rr = f->rng.as<PcgStream>() + 1;
+  w.err = sm.err; w.degenerate = sm.stats + 2;
+
+  int waves = 0;
+  for (int s0 = 0; s0 < cfg->spp; s0 += ns) {
+    w.s0 = s0;
+    w.ns = std::min(ns, cfg->spp - s0);
+    const int Pw = w.ns * n_own;
+    const int g = (Pw + 255) / 256;
+    camera_kernel<<<g, 256, 0, st>>>(f->F, C, w, S, Pw);
+    CUDA_TRY(cudaGetLastError());
+    if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st)) return rc;
+    after_primary_kernel<<<g, 256, 0, st>>>(w, S, Pw);
+    for (int b = 0; b < cfg->bounces; ++b) {
+      if (cfg->rr_start >= 0 && b >= cfg->rr_start) roulette_kernel<<<g, 256, 0, st>>>(w, S, Pw, b);
+      int rc = compact_flags(f, S.alive, f->F.n_obj > 1 ? S.obj : nullptr, Pw, f->F.n_obj, f->list.as<int>(),
+                             sm.seg, sm.count2, sm.stats + 1, st);
+      if (rc) return rc;
+      BounceOp op{};
+      op.list = f->list.as<int>(); op.count = sm.count2; op.n = Pw;
+      op.seg = f->F.n_obj > 1 ? sm.seg : nullptr;
+      if (f->F.n_obj == 1) op.seg = nullptr;
+      op.F = f->F_dev; op.S = S; op.w = w; op.backoff = f->F.backoff; op.b = b;
+      if ((rc = run_mlp(f, f->F, op, Pw, true, st))) return rc;
+      if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st))) return rc;
+      after_bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(w, S, f->list.as<int>(), sm.count2);
+    }
+    film_kernel<<<(n_own + 255) / 256, 256, 0, st>>>(w, S, accum);
+    CUDA_TRY(cudaGetLastError());
+    ++waves;
+  }
+  int host_small[32 + 8];
+  CUDA_TRY(cudaMemcpyAsync(host_small, f->small.p, sizeof(host_small), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const unsigned long long* hs64 = reinterpret_cast<const unsigned long long*>(host_small + 32);
+  if (stats) {
+    stats->forward_rows = hs64[0];
+    stats->gradient_rows = hs64[1];
+    stats->degenerate = hs64[2];
+    stats->path_samples = (uint64_t)n_own * cfg->spp;
+    stats->waves = waves;
+  }
+  if (host_small[18] & DEVERR_SIGN_RULE) return fail(DDF_ENUMERIC, "normal sign rule violated: n . dir >= 0");
+  return DDF_OK;
+}
+
+namespace {
+__global__ void rng_kernel(const PcgStream* st, const uint64_t* idx, int n, double* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) out[j] = pcg_single(*st, idx[j]);
+}
+struct CompactScratch {
+  Buf blocks, seg;
+};
+CompactScratch g_cs;
+}  // namespace
+
+int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64_t* idx, int64_t n, double* out,
+                    void* stream) {
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad count");
+  if (n == 0) return DDF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  PcgStream hs;
+  build_stream(state, inc, &hs);
+  PcgStream* d = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(hs), st));
+  CUDA_TRY(cudaMemcpyAsync(d, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+  rng_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(d, idx, (int)n, out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(d, st));
+  CUDA_TRY(cudaStreamSynchronize(st));   // hs lives on this stack frame
+  return DDF_OK;
+}
+
+int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, void* stream) {
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad count");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = std::max<int>(1, (int)((n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS));
+  CUDA_TRY(g_cs.blocks.ensure(sizeof(int) * nb));
+  CUDA_TRY(g_cs.seg.ensure(sizeof(int) * 2));
+  compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, (int)n, 1, g_cs.blocks.as<int>());
+  compact::scan_kernel<<<1, 1024, 0, st>>>(g_cs.blocks.as<int>(), nb, 1, g_cs.seg.as<int>(), count, nullptr);
+  compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, (int)n, 1, g_cs.blocks.as<int>(), list);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DDF_OK;
+}
+
+}  // extern "C"

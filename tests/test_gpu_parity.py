@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path through the C ABI vs the pinned CPU oracle and the
+reference's golden fixtures.
+
+Tolerances:
+  fp32 distances / gradients  |d| <= 1e-4 * max(|ref|, rms(ref))
+  hit masks                   >= 99.9 % identical
+  RNG draws, compaction       bit-exact
+  fp32 image (config 2)       RMSE <= 3e-3 (probe: 1.35e-3)
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import cpu_ddf as O  # noqa: E402
+from paper_2306_16142_b200 import _lib  # noqa: E402
+from paper_2306_16142_b200.field import CudaNeuralField  # noqa: E402
+from paper_2306_16142_b200.neural import MlpModel, kaiming_uniform  # noqa: E402
+from paper_2306_16142_b200 import render as R  # noqa: E402
+
+CFG_DELTA = 10.0 / 0.98
+BOX = np.array([[-1.0] * 3, [1.0] * 3])
+FP32_TOL = 1e-4
+
+
+def as_model(net):
+    return MlpModel(net.widths, net.v, net.g, net.b)
+
+
+def rel_err(x, ref):
+    scale = np.maximum(np.abs(ref), np.sqrt(np.mean(ref ** 2)))
+    return np.max(np.abs(x - ref) / scale)
+
+
+def march_net():
+    net = O.kaiming_uniform_net((5, 64, 64, 1), seed=7)
+    net.g[-1] = net.g[-1] * 0.05
+    net.b[-1] = net.b[-1] + 0.12
+    return net
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    net = O.kaiming_uniform_net((5, 128, 128, 128, 128, 1), 0)
+    return net, CudaNeuralField(as_model(net), CFG_DELTA, bounds=BOX)
+
+
+def test_library_is_native():
+    L = _lib.lib()
+    assert L._name.endswith("libddf_b200.so")
+
+
+def test_forward_batch_fp32(golden, cfg1):
+    _, f = cfg1
+    y = f.forward_inputs(golden["q_inputs"])
+    assert rel_err(y, golden["q_forward"]) <= FP32_TOL
+
+
+def test_input_gradient_fp32(golden, cfg1):
+    _, f = cfg1
+    g = f.input_gradient_inputs(golden["q_inputs"])
+    ref = golden["q_grad"]
+    for j in range(5):
+        assert rel_err(g[:, j], ref[:, j]) <= FP32_TOL
+
+
+def test_query_batch(golden, cfg1):
+    _, f = cfg1
+    pred, t, hit, _ = f.query_raw(golden["q_origins"], golden["q_dirs"])
+    assert rel_err(pred, golden["q_forward"]) <= FP32_TOL   # same inputs after re-canonicalisation
+    assert (hit == golden["q_query_hit"]).mean() >= 0.999
+    both = hit & golden["q_query_hit"]
+    assert rel_err(t[both], golden["q_query_t"][both]) <= FP32_TOL
+
+
+def test_trace_batch(golden, cfg1):
+    _, f = cfg1
+    t, hit = f.trace_batch(golden["q_trace_origins"], golden["q_dirs"])
+    assert (hit == golden["q_trace_hit"]).mean() >= 0.999
+    both = hit & golden["q_trace_hit"]
+    assert np.all(np.isinf(t[~hit]))
+    assert rel_err(t[both], golden["q_trace_t"][both]) <= FP32_TOL
+
+
+def test_trace_multistep_march(golden):
+    f = CudaNeuralField(as_model(march_net()), 0.1, bounds=BOX)
+    t, hit = f.trace_batch(golden["m_origins"], golden["m_dirs"])
+    assert (hit == golden["m_trace_hit"]).mean() >= 0.99
+    both = hit & golden["m_trace_hit"]
+    assert np.max(np.abs(t[both] - golden["m_trace_t"][both])) <= 1e-4
+
+
+def test_normal_batch(golden, cfg1):
+    _, f = cfg1
+    o = golden["q_trace_origins"]
+    th = np.where(np.isfinite(golden["q_trace_t"]), golden["q_trace_t"], 0.0)
+    n, v = f.normal_batch(o, golden["q_dirs"], t_hit=th)
+    assert (v == golden["q_normal_valid"]).all()
+    cosang = np.clip(np.einsum("ij,ij->i", n, golden["q_normal"]), -1, 1)
+    assert np.degrees(np.arccos(cosang)).max() < 0.05
+    assert np.all(np.einsum("ij,ij->i", n, golden["q_dirs"]) <= 0.0)
+
+
+def test_rng_bit_exact(golden):
+    s, inc = O.pcg_seed_state(42)
+    st = (ctypes.c_uint64 * 2)(s & (2**64 - 1), s >> 64)
+    ic = (ctypes.c_uint64 * 2)(inc & (2**64 - 1), inc >> 64)
+    far = [3 * 2 * 16384 * 5 + 12345, 2**40 + 7]
+    idx = torch.tensor(list(range(64)) + far, dtype=torch.int64, device="cuda")
+    out = torch.empty(len(idx), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().ddf_rng_doubles(st, ic, ctypes.c_void_p(idx.data_ptr()), len(idx),
+                                          ctypes.c_void_p(out.data_ptr()), None))
+    got = out.cpu().numpy()
+    assert np.array_equal(got[:64], golden["rng_first"])
+    for j, k in enumerate(far):
+        assert got[64 + j] == O.pcg_double((s, inc), k)
+
+
+@pytest.mark.parametrize("n", [0, 1, 1023, 1024, 1025, 70001])
+def test_compaction_bit_exact(n):
+    rng = np.random.default_rng(n)
+    flags = (rng.random(n) < 0.37).astype(np.uint8)
+    if n > 10:
+        flags[:5] = 1
+        flags[-3:] = 0
+    fd = torch.from_numpy(flags).cuda() if n else torch.empty(0, dtype=torch.uint8, device="cuda")
+    lst = torch.full((max(n, 1),), -1, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().ddf_compact(ctypes.c_void_p(fd.data_ptr()), n, ctypes.c_void_p(lst.data_ptr()),
+                                      ctypes.c_void_p(cnt.data_ptr()), None))
+    c = int(cnt.item())
+    ref = np.nonzero(flags)[0]
+    assert c == len(ref)
+    assert np.array_equal(lst.cpu().numpy()[:c], ref)
+
+
+def _cam(w, h):
+    return R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4.0, width=w, height=h)
+
+
+def test_render_config2_fp32(golden):
+    """Config 2 at full size: 128x128, 4 spp, 2 bounces, 5->8x256->1, seed 42."""
+    net = kaiming_uniform((5,) + (256,) * 8 + (1,), 1)
+    f = CudaNeuralField(net, CFG_DELTA, bounds=BOX)
+    cfg = R.RenderConfig(mode="path", spp=4, bounces=2, albedo=0.7, env_radiance=1.0, seed=42)
+    fb = R.render_path(f, _cam(128, 128), cfg)
+    img = fb.data[:, :, 0]
+    ref = golden["r2_film"]
+    rmse = np.sqrt(np.mean((img - ref) ** 2))
+    assert rmse <= 3e-3, rmse
+    assert np.mean(np.abs(img - ref) > 1e-9) < 0.01
+    fb2 = R.render_path(f, _cam(128, 128), cfg)
+    assert np.array_equal(fb2.data, fb.data)   # same seed, identical image
+
+
+def test_render_march_regime(golden):
+    f = CudaNeuralField(as_model(march_net()), 0.1, bounds=BOX)
+    cfg = R.RenderConfig(mode="path", spp=3, bounces=3, albedo=0.6, env_radiance=1.5, seed=9)
+    img = R.render_path(f, _cam(20, 12), cfg).data[:, :, 0]
+    ref = golden["rm_film"]
+    assert np.sqrt(np.mean((img - ref) ** 2)) <= 3e-2
+
+
+def test_render_matches_oracle_small_with_waves():
+    """Wave splitting (several spp per wave vs one) must not change the film."""
+    net = kaiming_uniform((5, 64, 64, 64, 1), 3)
+    f = CudaNeuralField(net, CFG_DELTA, bounds=BOX)
+    cam = _cam(33, 17)
+    cfg = R.RenderConfig(mode="path", spp=5, bounces=3, albedo=0.7, env_radiance=1.0, seed=5)
+    a = R.render_path(f, cam, cfg).data
+    cfg.max_wave_paths = 33 * 17 * 2
+    b = R.render_path(f, cam, cfg).data
+    assert np.array_equal(a, b)
+    onet = O.Net(net.widths, net.v, net.g, net.b)
+    ref = O.render_path(O.Field([onet], CFG_DELTA, bounds=BOX), O.Cam((0, 0, 3.0), (0, 0, 0.0), vfov=np.pi / 4,
+                                                                      width=33, height=17),
+                        O.PathConfig(spp=5, bounces=3, albedo=0.7, env=1.0, seed=5))
+    assert np.sqrt(np.mean((a[:, :, 0].reshape(-1) - ref) ** 2)) <= 3e-3
+
+
+def test_tile_sharding_sums_to_full_film():
+    net = kaiming_uniform((5, 64, 64, 1), 4)
+    f = CudaNeuralField(net, CFG_DELTA, bounds=BOX)
+    cam = _cam(150, 70)
+    full, _ = R.render_path_device(f, cam, R.RenderConfig(spp=2, bounces=2, seed=11))
+    full = full.cpu().numpy()
+    for world in (2, 3, 8):
+        acc = np.zeros_like(full)
+        for rank in range(world):
+            part, _ = R.render_path_device(f, cam, R.RenderConfig(spp=2, bounces=2, seed=11, tile=64, rank=rank,
+                                                                  world=world))
+            part = part.cpu().numpy()
+            assert np.all((part == 0) | (acc == 0))
+            acc += part
+        assert np.array_equal(acc, full)
+
+
+def test_errors_map_to_reference_classes(cfg1):
+    _, f = cfg1
+    with pytest.raises(ValueError):
+        R.render_path(f, _cam(8, 8), R.RenderConfig(spp=1, bounces=0))
