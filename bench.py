@@ -1,0 +1,325 @@
+"""Benchmark of the DDF path-tracing hot path on B200 (contract: see DESIGN.md).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+A step is one full render (render.render_path) of the chosen BASELINE config
+with inputs (weights, camera, RNG seed state) resident on the device; under
+torchrun each rank renders its 64x64 tiles and the film is summed over NCCL.
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the reference
+algorithm's CPU implementation (the float64 numpy oracle port, all host
+threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_CONFIG = "c2"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
+    ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- CPU side
+def oracle_field(name):
+    from oracle import cpu_ddf as O
+    from paper_2306_16142_b200 import configs as C
+    nets = [O.Net(m.widths, m.v, m.g, m.b) for m in C.models(name)]
+    w = C.WORKLOADS[name]
+    if w.get("scene"):
+        centers, scale, albedos = C.scene_layout()
+        return O.Field(nets, C.CFG_DELTA, bounds=C.SCENE_BOX, centers=centers, scale=scale, albedos=albedos)
+    return O.Field(nets, C.CFG_DELTA, bounds=C.UNIT_BOX)
+
+
+def cpu_sample_bands(name):
+    """Bounded CPU sample: pixel-row bands spread over the film at spp = 1
+    (the stream prefix of sample 0), sized for ~10-30 s on 8 cores."""
+    from paper_2306_16142_b200 import configs as C
+    w = C.WORKLOADS[name]
+    W, H = w["W"], w["H"]
+    if name == "c2":
+        return [(0, W * H)], w["spp"], "full render (128x128, 4 spp)"
+    rows_total = {"c3": 32, "c4": 8, "c5": 16}[name]
+    nb = 8
+    per = max(1, rows_total // nb)
+    bands = []
+    for b in range(nb):
+        y0 = int((b + 0.5) * H / nb) - per // 2
+        bands.append((y0 * W, (y0 + per) * W))
+    return bands, 1, f"{nb} bands x {per} rows x {W} px at spp=1 (stream prefix of sample 0)"
+
+
+def cpu_render_sample(name):
+    """One timed CPU step: (path samples, seconds)."""
+    from oracle import cpu_ddf as O
+    from paper_2306_16142_b200 import configs as C
+    w = C.WORKLOADS[name]
+    fld = oracle_field(name)
+    cam = O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=w["W"], height=w["H"])
+    bands, spp, _ = cpu_sample_bands(name)
+    cfg = O.PathConfig(spp=spp, bounces=w["bounces"], albedo=0.7, env=1.0, seed=C.RENDER_SEED,
+                       rr_start=w.get("rr_start", -1))
+    t0 = time.perf_counter()
+    n = 0
+    for a, b in bands:
+        O.render_path(fld, cam, cfg, pix_range=(a, b))
+        n += (b - a) * spp
+    return n, time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        nthr = max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:
+        nthr = os.cpu_count()
+    return int(nthr)
+
+
+def cpu_baseline(name, runs=1):
+    _, _, desc = cpu_sample_bands(name)
+    cpu_render_sample(name) if name != "c2" else None   # warm-up (BLAS threads, page-in)
+    vals = []
+    for _ in range(runs):
+        n, s = cpu_render_sample(name)
+        vals.append(n / s)
+    return {"value": statistics.median(vals), "unit": "path_samples/s", "cores": cpu_cores(), "kind": "port",
+            "sample": desc + "; float64 numpy oracle (oracle/cpu_ddf.py), OpenBLAS threads"}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 8:
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- GPU side
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    name = args.config
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from paper_2306_16142_b200 import configs as C
+        w = C.WORKLOADS[name]
+        _, _, desc = cpu_sample_bands(name)
+        for _ in range(args.warmup):
+            cpu_render_sample(name)
+        tot_n, tot_s = 0, 0.0
+        for _ in range(args.steps):
+            n, s = cpu_render_sample(name)
+            tot_n += n
+            tot_s += s
+        v = tot_n / tot_s
+        print(json.dumps({
+            "impl": "reference", "metric": "path_samples_per_s", "value": v, "unit": "path_samples/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "W": w["W"], "H": w["H"], "spp": w["spp"], "bounces": w["bounces"],
+                       "sample": desc},
+            "cpu_baseline": {"value": v, "unit": "path_samples/s", "cores": cpu_cores(), "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": "path_samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2306_16142_b200 import configs as C
+    from paper_2306_16142_b200 import render as R
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = C.WORKLOADS[name]
+    prec = args.precision or w["precision"]
+    fld = C.build_field(name, precision=prec)
+    cam = C.camera(name)
+    cfg = C.render_config(name, rank=rank, world=world)
+    n_pix = cam.width * cam.height
+    accum = torch.empty(n_pix, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step(profile=0):
+        cfg.profile = profile
+        _, st = R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
+        if world > 1:
+            dist.all_reduce(accum, op=dist.ReduceOp.SUM)
+        return st
+
+    for _ in range(max(3, args.warmup)):
+        st = step()
+    torch.cuda.synchronize()
+
+    per_step = []
+    launches = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per_step.append(e0.elapsed_time(e1))
+            launches += st["kernel_launches"]
+    ms_local = float(np.mean(per_step))
+    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    samples_total = n_pix * cfg.spp
+    value = samples_total / (ms / 1e3)
+
+    # kernel-class breakdown (one profiled render; CUDA events on the launch stream)
+    stp = step(profile=1)
+    torch.cuda.synchronize()
+    models = C.models(name)
+    F = sum(C.mlp_flops(m.widths) for m in models) if w.get("scene") else C.mlp_flops(models[0].widths)
+    F_grad = 2 * C.mlp_flops(models[0].widths)   # one object's network per gradient row
+    fwd_flops = F * stp["forward_rows"]
+    grad_flops = F_grad * stp["gradient_rows"]
+    mlp_ms = stp["ms_forward"] + stp["ms_gradient"]
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak_tf = float(peaks.get("bf16_tflops", 1590.0))
+    achieved_tf = (fwd_flops + grad_flops) / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else 0.0
+    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved_tf / peak_tf, "traffic": None,
+                "kernel": "fused DDF-MLP (forward trace-step + input-gradient bounce)",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1590",
+                "mlp_share_of_step": mlp_ms / stp["ms_total"] if stp["ms_total"] else None,
+                "forward": {"rows": stp["forward_rows"], "ms": stp["ms_forward"], "launches": stp["forward_launches"],
+                            "tflops": fwd_flops / (stp["ms_forward"] / 1e3) / 1e12 if stp["ms_forward"] else None},
+                "gradient": {"rows": stp["gradient_rows"], "ms": stp["ms_gradient"],
+                             "launches": stp["gradient_launches"],
+                             "tflops": grad_flops / (stp["ms_gradient"] / 1e3) / 1e12 if stp["ms_gradient"] else None},
+                "compaction_ms": stp["ms_compact"], "other_ms": stp["ms_other"], "profiled_step_ms": stp["ms_total"]}
+
+    # end to end through the public API: host film out, RNG tables in
+    e2e = None
+    if not args.no_e2e:
+        ts = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            acc, _ = R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
+            if world > 1:
+                dist.reduce(acc, dst=0, op=dist.ReduceOp.SUM)
+            if rank == 0:
+                R.film_from_accum(acc, cam, cfg.spp)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        te = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": samples_total / te.item(), "unit": "path_samples/s",
+               "h2d_bytes_per_step": 2 * (16 + 64 * 32) + 0,   # PCG64 jump tables (camera/config are kernel params)
+               "d2h_bytes_per_step": n_pix * 8 + 160}
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_baseline:
+        cpu = cpu_baseline(name)
+
+    if rank == 0:
+        out = {
+            "metric": "path_samples_per_s", "value": value, "unit": "path_samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": {"workload": name, "W": cam.width, "H": cam.height, "spp": cfg.spp, "bounces": cfg.bounces,
+                       "widths": list(models[0].widths), "n_networks": len(models), "precision": prec,
+                       "tiles": cfg.tile, "parallelism": f"tiles{world}" if world > 1 else "single",
+                       "l2": "flushed (256 MB write) between timed steps"},
+            "ddf_queries_per_s": stp["forward_rows"] / (ms / 1e3),
+            "gradient_rows_per_s": stp["gradient_rows"] / (ms / 1e3),
+            "flops_per_step": fwd_flops + grad_flops,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -65,6 +65,8 @@ typedef struct {
   int32_t tile, rank, world;
   /* path slots per wave (0 = default); larger waves mean fewer launches */
   int64_t max_wave_paths;
+  /* 1: time every kernel class with CUDA events on `stream` (stats.ms_*) */
+  int32_t profile;
 } ddf_path_config_t;
 
 typedef struct {
@@ -73,6 +75,10 @@ typedef struct {
   uint64_t degenerate;     /* normals that fell back to -d (render.py:133)  */
   uint64_t path_samples;   /* owned pixels x spp                            */
   int32_t waves;
+  uint64_t kernel_launches;     /* every kernel this call launched           */
+  uint64_t forward_launches, gradient_launches;
+  /* profile = 1 only: summed CUDA-event durations per kernel class */
+  double ms_forward, ms_gradient, ms_compact, ms_other, ms_total;
 } ddf_render_stats_t;
 
 /* NeuralField.__init__ (field.py:231-237): delta, AABB bounds (lo xyz, hi xyz). */

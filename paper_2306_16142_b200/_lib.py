@@ -66,13 +66,16 @@ class PathConfig_t(ctypes.Structure):
                 ("rr_start", ctypes.c_int32),
                 ("rr_state", ctypes.c_uint64 * 2), ("rr_inc", ctypes.c_uint64 * 2),
                 ("tile", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("max_wave_paths", ctypes.c_int64)]
+                ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32)]
 
 
 class RenderStats_t(ctypes.Structure):
     _fields_ = [("forward_rows", ctypes.c_uint64), ("gradient_rows", ctypes.c_uint64),
                 ("degenerate", ctypes.c_uint64), ("path_samples", ctypes.c_uint64),
-                ("waves", ctypes.c_int32)]
+                ("waves", ctypes.c_int32), ("kernel_launches", ctypes.c_uint64),
+                ("forward_launches", ctypes.c_uint64), ("gradient_launches", ctypes.c_uint64),
+                ("ms_forward", ctypes.c_double), ("ms_gradient", ctypes.c_double),
+                ("ms_compact", ctypes.c_double), ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double)]
 
 
 _lib = None

@@ -1,0 +1,98 @@
+"""The BASELINE.json configs as concrete synthetic workloads.
+
+Every config uses the pinhole camera at (0, 0, 3) looking at the origin with a
+45 degree vertical field of view, delta = 10/0.98 (hit threshold exactly 10.0,
+SURVEY App. A), Lambertian albedo 0.7, constant white environment, and
+Kaiming-uniform weights with zero biases from the stated seed.
+
+  c1  query batch: 65,536 rays, 5->4x128->1 fp32, seed 0
+  c2  render 128x128, 4 spp, 2 bounces, 5->8x256->1 fp32, seed 1, PCG seed 42
+  c3  render 512x512, 16 spp, 4 bounces, 65->8x512->1 bf16, seed 2
+  c4  render 1920x1080, 64 spp, 8 bounces, RR from bounce 3, 65->8x512->1
+      bf16 (seed 2), 64x64 tiles round-robin over ranks
+  c5  render 1024x1024, 32 spp, 6 bounces, 8 x (65->6x256->1) seeds 10-17 at
+      (+-0.75)^3, scale 0.5, albedos U[0.2, 0.9] from default_rng(5), bounds
+      [-1.25, 1.25]^3, bf16
+"""
+
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+from .neural import kaiming_uniform
+
+CFG_DELTA = 10.0 / 0.98
+UNIT_BOX = np.array([[-1.0, -1.0, -1.0], [1.0, 1.0, 1.0]])
+SCENE_BOX = np.array([[-1.25, -1.25, -1.25], [1.25, 1.25, 1.25]])
+RENDER_SEED = 42
+
+WORKLOADS = {
+    "c1": dict(kind="query", widths=(5, 128, 128, 128, 128, 1), net_seed=0, n=65536, precision="fp32"),
+    "c2": dict(kind="render", widths=(5,) + (256,) * 8 + (1,), net_seed=1, W=128, H=128, spp=4, bounces=2,
+               precision="fp32"),
+    "c3": dict(kind="render", widths=(65,) + (512,) * 8 + (1,), net_seed=2, W=512, H=512, spp=16, bounces=4,
+               precision="bf16"),
+    "c4": dict(kind="render", widths=(65,) + (512,) * 8 + (1,), net_seed=2, W=1920, H=1080, spp=64, bounces=8,
+               rr_start=3, tile=64, precision="bf16"),
+    "c5": dict(kind="render", widths=(65,) + (256,) * 6 + (1,), net_seed=None, W=1024, H=1024, spp=32, bounces=6,
+               scene=True, precision="bf16"),
+}
+
+
+def mlp_flops(widths) -> int:
+    """Algorithmic forward FLOPs per query: 2 * sum in_l * out_l."""
+    return 2 * sum(a * b for a, b in zip(widths[:-1], widths[1:]))
+
+
+def scene_layout():
+    """Config 5: 8 objects on a 2x2x2 grid of spacing 1.5, scale 0.5."""
+    centers = np.array([c for c in itertools.product((-0.75, 0.75), repeat=3)], dtype=np.float64)
+    albedos = np.random.default_rng(5).uniform(0.2, 0.9, 8)
+    return centers, 0.5, albedos
+
+
+def models(name):
+    w = WORKLOADS[name]
+    if w.get("scene"):
+        return [kaiming_uniform(w["widths"], s) for s in range(10, 18)]
+    return [kaiming_uniform(w["widths"], w["net_seed"])]
+
+
+def query_rays(n: int, seed: int = 0):
+    """Config 1 rays: origins U[-1,1]^3 then directions = normalised N(0, I3),
+    both from default_rng(seed)."""
+    rng = np.random.default_rng(seed)
+    o = rng.uniform(-1.0, 1.0, (n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return o, d
+
+
+def camera(name):
+    from .render import Camera
+    w = WORKLOADS[name]
+    return Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4.0, width=w["W"], height=w["H"])
+
+
+def render_config(name, rank: int = 0, world: int = 1, **over):
+    from .render import RenderConfig
+    w = WORKLOADS[name]
+    cfg = RenderConfig(mode="path", spp=w["spp"], bounces=w["bounces"], albedo=0.7, env_radiance=1.0,
+                       seed=RENDER_SEED, rr_start=w.get("rr_start", -1), tile=w.get("tile", 64 if world > 1 else 0),
+                       rank=rank, world=world)
+    for k, v in over.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+def build_field(name, precision: str | None = None):
+    from .field import CudaNeuralField
+    w = WORKLOADS[name]
+    prec = precision or w["precision"]
+    ms = models(name)
+    if w.get("scene"):
+        centers, scale, albedos = scene_layout()
+        return CudaNeuralField.scene(ms, centers, scale, albedos, CFG_DELTA, bounds=SCENE_BOX, precision=prec)
+    return CudaNeuralField(ms[0], CFG_DELTA, bounds=UNIT_BOX, precision=prec)

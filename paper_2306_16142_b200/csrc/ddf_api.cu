@@ -54,7 +54,42 @@ struct Buf {
 
 }  // namespace
 
+// Per-call kernel-class timing (cfg->profile) and launch counting.
+struct Prof {
+  enum { FWD = 0, GRAD = 1, COMPACT = 2, OTHER = 3, TOTAL = 4, NCAT = 5 };
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<size_t, size_t>> marks[NCAT];
+  uint64_t launches = 0, fwd_launches = 0, grad_launches = 0;
+  void reset(bool enable) {
+    on = enable;
+    used = 0;
+    for (auto& m : marks) m.clear();
+    launches = fwd_launches = grad_launches = 0;
+  }
+  size_t rec(cudaStream_t st) {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    cudaEventRecord(pool[used], st);
+    return used++;
+  }
+  double total_ms(int cat) {
+    double t = 0.0;
+    for (auto& m : marks[cat]) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pool[m.first], pool[m.second]);
+      t += ms;
+    }
+    return t;
+  }
+};
+
 struct ddf_field_s {
+  Prof prof;
   FieldDev F{};                 // host copy holding device pointers
   FieldDev* F_dev = nullptr;    // device copy (BounceOp reads albedos through it)
   std::vector<void*> weights;   // device weight allocations
@@ -114,9 +149,19 @@ int launch_simt(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, b
   return DDF_OK;
 }
 
+// RAII marker: records start/stop events of one kernel-class region
+struct ProfScope {
+  Prof& p; int cat; cudaStream_t st; size_t a = 0;
+  ProfScope(Prof& p_, int c, cudaStream_t s) : p(p_), cat(c), st(s) { if (p.on) a = p.rec(st); }
+  ~ProfScope() { if (p.on) p.marks[cat].push_back({a, p.rec(st)}); }
+};
+
 template <class Op>
 int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool grad, cudaStream_t st) {
   if (max_rows <= 0) return DDF_OK;
+  ProfScope ps(f->prof, grad ? Prof::GRAD : Prof::FWD, st);
+  f->prof.launches += 1;
+  (grad ? f->prof.grad_launches : f->prof.fwd_launches) += 1;
   if (F.precision == PREC_BF16) return umma::launch<Op>(F, op, max_rows, grad, f->sm_count, st, &g_err);
   const int w = max_width(F);
   if (w <= 256) return launch_simt<Op, 64, 256>(f, F, op, max_rows, grad, st);
@@ -131,6 +176,8 @@ int compact_flags(ddf_field_s* f, const uint8_t* flags, const int* obj, int n, i
   CUDA_TRY(f->blocks.ensure(sizeof(int) * nb * DDF_MAX_OBJECTS));
   int* bc = f->blocks.as<int>();
   const int no = obj ? n_obj : 1;
+  ProfScope ps(f->prof, Prof::COMPACT, st);
+  f->prof.launches += 3;
   compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, obj, n, no, bc);
   compact::scan_kernel<<<1, 1024, 0, st>>>(bc, nb, no, seg, count, rows_acc);
   compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, obj, n, no, bc, list);
@@ -436,6 +483,8 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   CUDA_TRY(cudaSetDevice(f->device));
   if (int rc = ensure_small(f)) return rc;
   Small sm = small_of(f);
+  f->prof.reset(cfg->profile != 0);
+  size_t t_begin = f->prof.on ? f->prof.rec(st) : 0;
 
   // owned pixels, ascending global index (cached per film/sharding)
   const int key[6] = {cam->width, cam->height, cfg->tile, cfg->rank, cfg->world, 1};
@@ -465,6 +514,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   CUDA_TRY(cudaMemsetAsync(f->small.p, 0, 4096, st));
   if (n_own == 0) {
     if (stats) std::memset(stats, 0, sizeof(*stats));
+    f->prof.reset(false);
     return DDF_OK;
   }
 
@@ -523,12 +573,24 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     w.ns = std::min(ns, cfg->spp - s0);
     const int Pw = w.ns * n_own;
     const int g = (Pw + 255) / 256;
-    camera_kernel<<<g, 256, 0, st>>>(f->F, C, w, S, Pw);
+    {
+      ProfScope ps(f->prof, Prof::OTHER, st);
+      camera_kernel<<<g, 256, 0, st>>>(f->F, C, w, S, Pw);
+      f->prof.launches += 1;
+    }
     CUDA_TRY(cudaGetLastError());
     if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st)) return rc;
-    after_primary_kernel<<<g, 256, 0, st>>>(w, S, Pw);
+    {
+      ProfScope ps(f->prof, Prof::OTHER, st);
+      after_primary_kernel<<<g, 256, 0, st>>>(w, S, Pw);
+      f->prof.launches += 1;
+    }
     for (int b = 0; b < cfg->bounces; ++b) {
-      if (cfg->rr_start >= 0 && b >= cfg->rr_start) roulette_kernel<<<g, 256, 0, st>>>(w, S, Pw, b);
+      if (cfg->rr_start >= 0 && b >= cfg->rr_start) {
+        ProfScope ps(f->prof, Prof::OTHER, st);
+        roulette_kernel<<<g, 256, 0, st>>>(w, S, Pw, b);
+        f->prof.launches += 1;
+      }
       int rc = compact_flags(f, S.alive, f->F.n_obj > 1 ? S.obj : nullptr, Pw, f->F.n_obj, f->list.as<int>(),
                              sm.seg, sm.count2, sm.stats + 1, st);
       if (rc) return rc;
@@ -539,12 +601,21 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
       op.F = f->F_dev; op.S = S; op.w = w; op.backoff = f->F.backoff; op.b = b;
       if ((rc = run_mlp(f, f->F, op, Pw, true, st))) return rc;
       if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st))) return rc;
-      after_bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(w, S, f->list.as<int>(), sm.count2);
+      {
+        ProfScope ps(f->prof, Prof::OTHER, st);
+        after_bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(w, S, f->list.as<int>(), sm.count2);
+        f->prof.launches += 1;
+      }
     }
-    film_kernel<<<(n_own + 255) / 256, 256, 0, st>>>(w, S, accum);
+    {
+      ProfScope ps(f->prof, Prof::OTHER, st);
+      film_kernel<<<(n_own + 255) / 256, 256, 0, st>>>(w, S, accum);
+      f->prof.launches += 1;
+    }
     CUDA_TRY(cudaGetLastError());
     ++waves;
   }
+  if (f->prof.on) f->prof.marks[Prof::TOTAL].push_back({t_begin, f->prof.rec(st)});
   int host_small[32 + 8];
   CUDA_TRY(cudaMemcpyAsync(host_small, f->small.p, sizeof(host_small), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -555,6 +626,14 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     stats->degenerate = hs64[2];
     stats->path_samples = (uint64_t)n_own * cfg->spp;
     stats->waves = waves;
+    stats->kernel_launches = f->prof.launches;
+    stats->forward_launches = f->prof.fwd_launches;
+    stats->gradient_launches = f->prof.grad_launches;
+    stats->ms_forward = f->prof.total_ms(Prof::FWD);
+    stats->ms_gradient = f->prof.total_ms(Prof::GRAD);
+    stats->ms_compact = f->prof.total_ms(Prof::COMPACT);
+    stats->ms_other = f->prof.total_ms(Prof::OTHER);
+    stats->ms_total = f->prof.total_ms(Prof::TOTAL);
   }
   if (host_small[18] & DEVERR_SIGN_RULE) return fail(DDF_ENUMERIC, "normal sign rule violated: n . dir >= 0");
   return DDF_OK;

@@ -85,6 +85,7 @@ class RenderConfig:
     rank: int = 0
     world: int = 1
     max_wave_paths: int = 0
+    profile: int = 0            # 1: per-kernel-class CUDA-event timing in the stats
 
     def __post_init__(self):
         if self.spp < 1:
@@ -131,6 +132,7 @@ def path_struct(config) -> _lib.PathConfig_t:
     p.rank = int(getattr(config, "rank", 0))
     p.world = int(getattr(config, "world", 1))
     p.max_wave_paths = int(getattr(config, "max_wave_paths", 0))
+    p.profile = int(getattr(config, "profile", 0))
     return p
 
 
@@ -149,8 +151,7 @@ def render_path_device(backend, camera, config, accum=None, stream=None):
     _lib.check(_lib.lib().ddf_render_path(backend.handle, ctypes.byref(cam), ctypes.byref(cfg),
                                           ctypes.c_void_p(accum.data_ptr()), ctypes.byref(st),
                                           ctypes.c_void_p(s.cuda_stream)))
-    stats = {"forward_rows": st.forward_rows, "gradient_rows": st.gradient_rows,
-             "degenerate": st.degenerate, "path_samples": st.path_samples, "waves": st.waves}
+    stats = {k: getattr(st, k) for k, _ in _lib.RenderStats_t._fields_}
     return accum, stats
 
 
