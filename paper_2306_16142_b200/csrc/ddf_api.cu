@@ -99,7 +99,7 @@ struct ddf_field_s {
   // scratch
   Buf t_acc, t_exit, alive, list, list2, blocks, small, ones;
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
-  Buf pix, rng;
+  Buf pix, rng, umma_masks;
   int pix_key[6] = {-1, -1, -1, -1, -1, -1};
   int pix_n = 0;
 };
@@ -162,7 +162,19 @@ int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool 
   ProfScope ps(f->prof, grad ? Prof::GRAD : Prof::FWD, st);
   f->prof.launches += 1;
   (grad ? f->prof.grad_launches : f->prof.fwd_launches) += 1;
-  if (F.precision == PREC_BF16) return umma::launch<Op>(F, op, max_rows, grad, f->sm_count, st, &g_err);
+  if (F.precision == PREC_BF16) {
+    CUDA_TRY(f->umma_masks.ensure(sizeof(uint32_t) * (size_t)umma::MASK_WORDS_PER_CTA * f->sm_count));
+    std::vector<umma::NetImage> imgs;
+    if (F.n_obj == 1 && f->F.n_obj > 1) {
+      // single-network pass (ddf_mlp_*): find which image F.net[0] is
+      for (auto& im : f->images)
+        if (im.dev == F.net[0].wimg_fwd) imgs.push_back(im);
+    } else {
+      imgs = f->images;
+    }
+    int rc = umma::launch<Op>(F, imgs, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st, &g_err);
+    return rc ? (rc == 1 ? DDF_EUSAGE : DDF_ECUDA) : DDF_OK;
+  }
   const int w = max_width(F);
   if (w <= 256) return launch_simt<Op, 64, 256>(f, F, op, max_rows, grad, st);
   if (w <= 512) return launch_simt<Op, 32, 512>(f, F, op, max_rows, grad, st);
@@ -285,7 +297,7 @@ int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths
   if (widths[L] != 1) return fail(DDF_EDATA, "network head must have width 1");
   for (int l = 0; l < n_widths; ++l)
     if (widths[l] < 1) return fail(DDF_EDATA, "bad layer width");
-  if (encoding == DDF_ENC_RAW5 && widths[0] != 5) return fail(DDF_EDATA, "raw encoding needs 5 inputs");
+  if (encoding == DDF_ENC_RAW5 && widths[0] != 5) encoding = 2;   // raw-input ops only (ddf_mlp_*)
   if (encoding == DDF_ENC_PE6 && widths[0] != 65) return fail(DDF_EDATA, "PE encoding needs 65 inputs");
   if (!(scale > 0.0)) return fail(DDF_EUSAGE, "scale must be positive");
   CUDA_TRY(cudaSetDevice(f->device));
@@ -364,7 +376,7 @@ int ddf_field_destroy(ddf_field_t f) {
   for (auto& im : f->images) umma::free_image(&im);
   Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones,
                  &f->st_o, &f->st_d, &f->st_tacc, &f->st_texit, &f->st_t, &f->st_thr, &f->st_rad,
-                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng};
+                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks};
   for (Buf* b : bufs) b->release();
   if (f->F_dev) cudaFree(f->F_dev);
   delete f;

@@ -1,20 +1,663 @@
-// bf16 tcgen05 engine (placeholder until the UMMA kernels land).
+// bf16 DDF-MLP engine on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// One persistent CTA per SM, 128-row tiles (the UMMA M = 128 datapath), ten
+// warps:
+//   warp 0      weight producer: streams UMMA-ready weight chunks (pre-swizzled
+//               on the host) global->shared with cp.async.bulk + mbarrier tx
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (kind::f16,
+//               bf16 x bf16 -> fp32 in TMEM), commits to mbarriers
+//   warps 2-9   row warps: input encoding in registers -> A tile in shared
+//               memory; per layer the TMEM->register epilogue (bias + ReLU /
+//               ReLU masks / gradient masks) writes the next layer's bf16 A
+//               tile back into shared memory; the last epilogue hands the
+//               distance (or input gradient) to the row op.
+//
+// Activations never leave the SM.  Each dense layer is split into two
+// N-halves whose accumulators sit side by side in TMEM (<= 512 fp32 columns);
+// the epilogue of half 0 overwrites A columns [0, N/2) as soon as the MMAs of
+// half 1 have read them (a_free barriers), so one A buffer (128 x 512 bf16)
+// suffices and the tensor pipe stays busy while the epilogue runs.
+//
+// Gradient programs (neural.py:229-249) run the hidden layers forward storing
+// ReLU bit masks (one u32 per row per 32 columns, per-CTA global scratch),
+// seed d/dh of the last hidden layer with w_head * mask, then run the
+// backward chain d_h <- (d_h * mask) @ W on the tensor cores with W^T images.
 #pragma once
+#include <cstring>
 #include <string>
+#include <vector>
+
+#include <cuda_bf16.h>
+
 #include "ddf_common.cuh"
+#include "field_kernels.cuh"
+
 namespace ddf {
 namespace umma {
-struct NetImage { void* dev = nullptr; int in_width = 0; };
-inline int build_image(const int32_t* widths, int32_t, const double*, const double*, NetImage* img, std::string*) {
-  img->in_width = widths[0];
-  img->dev = nullptr;
+
+constexpr int ROWS = 128;
+constexpr int NTHREADS = 320;
+constexpr int EPI_WARP0 = 2;
+constexpr int N_EPI_WARPS = 8;
+constexpr int MASK_WORDS_PER_CTA = DDF_MAX_LAYERS * 16 * ROWS;   // u32: [layer][col/32][row]
+
+enum Epi : int { E_RELU_A = 0, E_HEAD = 1, E_RELU_MASK_A = 2, E_MASKG_A = 3, E_BWD_MASK_A = 4, E_BWD_OUT = 5 };
+__host__ __device__ inline bool writes_a(int e) { return e == E_RELU_A || e == E_RELU_MASK_A || e == E_MASKG_A || e == E_BWD_MASK_A; }
+
+struct Step {
+  int K, N, nh, epi;
+  int nchunk;          // 64-wide K chunks per half
+  int rows;            // N / nh (MMA N)
+  int chunk_bytes;     // rows * 128
+  int mask_layer;      // E_RELU_MASK_A: layer stored; E_BWD_MASK_A: layer applied
+  long long img_off;   // byte offset of the step's first chunk in the image
+  const float* bias;   // fp32 (N) or nullptr
+};
+
+struct Prog {
+  int n_fwd, n_grad;
+  int k0;              // padded input width (multiple of 16)
+  int in_width;        // unpadded input width
+  int encoding;
+  int kmax;            // widest A tile (columns)
+  int max_chunk_bytes;
+  float head_b;
+  const float* head_w; // fp32, padded last hidden width
+  const uint8_t* img_fwd;
+  const uint8_t* img_grad;
+  Step fwd[DDF_MAX_LAYERS];
+  Step grad[2 * DDF_MAX_LAYERS];
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// K-major, 128-byte swizzled canonical layout: 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+  d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+  return d;
+}
+// kind::f16 instruction descriptor: bf16 A/B, fp32 D, K-major A and B, M = 128
+__device__ __forceinline__ uint32_t idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+#define DDF_TMEM_LD32(taddr, r)                                                                                   \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                              \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),          \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),    \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),  \
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])   \
+      : "r"(taddr))
+#define DDF_TMEM_LD16(taddr, r)                                                                                   \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"    \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),          \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])     \
+      : "r"(taddr))
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// byte offset of the 16-byte chunk (8 columns starting at col) of row r in a
+// [K/64][128 rows][128 B] swizzled A tile
+__device__ __forceinline__ uint32_t a_off(int r, int col) {
+  const int kb = col >> 6, cc = (col & 63) >> 3;
+  return (uint32_t)(kb * (ROWS * 128) + (r >> 3) * 1024 + (r & 7) * 128 + ((cc ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// ------------------------------------------------------------------ tiles
+// Forward: tile t covers list rows [128 t, 128 t + 128) and runs every object.
+// Gradient: tiles enumerate (object, 128-row block) over the object segments.
+template <class Op>
+__device__ __forceinline__ int n_tiles(const FieldDev& F, const Op& op) {
+  if constexpr (Op::kGrad) {
+    int t = 0;
+    for (int j = 0; j < F.n_obj; ++j) t += (op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS;
+    return t;
+  } else {
+    return (op.total() + ROWS - 1) / ROWS;
+  }
+}
+template <class Op>
+__device__ __forceinline__ void tile_rows(const FieldDev& F, const Op& op, int t, int& j0, int& j1, int& base, int& nv) {
+  if constexpr (Op::kGrad) {
+    int j = 0;
+    for (;; ++j) {
+      const int c = (op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS;
+      if (t < c || j == F.n_obj - 1) break;
+      t -= c;
+    }
+    base = op.seg_begin(j) + t * ROWS;
+    nv = min(ROWS, op.seg_end(j) - base);
+    j0 = j;
+    j1 = j + 1;
+  } else {
+    base = t * ROWS;
+    nv = min(ROWS, op.total() - base);
+    j0 = 0;
+    j1 = F.n_obj;
+  }
+}
+
+struct Smem {
+  uint8_t* a;           // A tile, 1024-aligned
+  uint8_t* stages;      // weight stages
+  uint64_t* bars;       // [0..1] a_ready, [2..3] acc_ready, [4..5] a_free, [6..6+S) w_full, [..+S) w_empty
+  uint32_t* tmem_slot;
+  float* red;           // [2][128] head partial sums
+};
+
+// ------------------------------------------------------------------ kernel
+template <class Op>
+__global__ void __launch_bounds__(NTHREADS, 1)
+mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int a_bytes,
+           int stage_bytes) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  Smem S;
+  S.a = base_ptr;
+  S.stages = base_ptr + a_bytes;
+  S.bars = reinterpret_cast<uint64_t*>(S.stages + (size_t)n_stages * stage_bytes);
+  S.tmem_slot = reinterpret_cast<uint32_t*>(S.bars + 6 + 2 * n_stages);
+  S.red = reinterpret_cast<float*>(S.tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar0 = smem_u32(S.bars);
+  auto BAR_A_READY = [&](int h) { return bar0 + 8u * (0 + h); };
+  auto BAR_ACC = [&](int h) { return bar0 + 8u * (2 + h); };
+  auto BAR_A_FREE = [&](int h) { return bar0 + 8u * (4 + h); };
+  auto BAR_FULL = [&](int s) { return bar0 + 8u * (6 + s); };
+  auto BAR_EMPTY = [&](int s) { return bar0 + 8u * (6 + n_stages + s); };
+
+  if (threadIdx.x == 0) {
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(BAR_A_READY(h), N_EPI_WARPS);
+      mbar_init(BAR_ACC(h), 1);
+      mbar_init(BAR_A_FREE(h), 1);
+    }
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(BAR_FULL(s), 1);
+      mbar_init(BAR_EMPTY(s), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(S.tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *S.tmem_slot;
+  const uint32_t a_base = smem_u32(S.a);
+  const uint32_t st_base = smem_u32(S.stages);
+  const int tiles = n_tiles(F, op);
+
+  if (warp == 0) {
+    // ================================================= weight producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int j0, j1, base, nv;
+        tile_rows(F, op, t, j0, j1, base, nv);
+        for (int j = j0; j < j1; ++j) {
+          const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+          const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
+          const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
+          for (int s = 0; s < ns; ++s) {
+            const Step& st = Op::kGrad ? P->grad[s] : P->fwd[s];
+            const uint8_t* src = img + st.img_off;
+            const int nck = st.nh * st.nchunk;
+            for (int c = 0; c < nck; ++c) {
+              mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
+              mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
+              bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+              src += st.chunk_bytes;
+              if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================= MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t ar[2] = {0u, 0u};
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int j0, j1, base, nv;
+        tile_rows(F, op, t, j0, j1, base, nv);
+        for (int j = j0; j < j1; ++j) {
+          const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+          const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
+          int prev_rows = 1 << 30;
+          for (int s = 0; s < ns; ++s) {
+            const Step& st = Op::kGrad ? P->grad[s] : P->fwd[s];
+            const uint32_t id = idesc(st.rows);
+            const bool wa = writes_a(st.epi);
+            const int c0 = min(st.nchunk - 1, ((st.N >> 1) - 1) >> 6);   // last chunk touching A cols < N/2
+            bool waited0 = false, waited1 = false;
+            if (st.rows > prev_rows) {
+              // half 0 of this step would overwrite TMEM columns of the previous
+              // step's half 1: wait until both previous epilogue halves are done
+              mbar_wait(BAR_A_READY(0), ar[0] & 1u); ++ar[0]; waited0 = true;
+              mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; waited1 = true;
+            }
+            prev_rows = st.rows;
+            for (int h = 0; h < st.nh; ++h) {
+              for (int kc = 0; kc < st.nchunk; ++kc) {
+                const bool need1 = (kc * 64 + 63) >= (st.K >> 1);
+                if (!waited0) { mbar_wait(BAR_A_READY(0), ar[0] & 1u); ++ar[0]; waited0 = true; }
+                if (need1 && !waited1) { mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; waited1 = true; }
+                mbar_wait(BAR_FULL(stage), phase);
+                tc_after_sync();
+                const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
+                const uint32_t a_chunk = a_base + (uint32_t)(kc * ROWS * 128);
+                const uint32_t b_chunk = st_base + (uint32_t)(stage * stage_bytes);
+                for (int ks = 0; ks < nks; ++ks) {
+                  mma_bf16(tmem + (uint32_t)(h * st.rows), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
+                           (kc | ks) ? 1u : 0u);
+                }
+                tc_commit(BAR_EMPTY(stage));
+                if (wa && h == st.nh - 1) {
+                  if (kc == c0) tc_commit(BAR_A_FREE(0));
+                  if (kc == st.nchunk - 1) tc_commit(BAR_A_FREE(1));
+                }
+                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              }
+              tc_commit(BAR_ACC(h));
+            }
+            if (!waited1) { mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; }   // keep phases in step
+          }
+        }
+      }
+    }
+  } else {
+    // ================================================= row warps (encoding + epilogues)
+    const int q = warp & 3;              // TMEM lane quarter of this warp
+    const int sub = (warp - EPI_WARP0) >> 2;   // column split between the two warps of a quarter
+    const int r = q * 32 + lane;         // tile row == TMEM lane
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    uint32_t* my_masks = mask_scratch + (size_t)blockIdx.x * MASK_WORDS_PER_CTA;
+    uint32_t acc_ph[2] = {0u, 0u}, free_ph[2] = {0u, 0u};
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int j0, j1, base, nv;
+      tile_rows(F, op, t, j0, j1, base, nv);
+      const bool valid = r < nv;
+      int slot = 0;
+      double pos[3] = {0.0, 0.0, 0.0}, az = 0.0, pol = 0.0;
+      if (valid) {
+        slot = op.slot(base + r);
+        if constexpr (!Op::kRaw) op.load(slot, pos, az, pol);
+      }
+      double best = 0.0;
+      int bobj = 0;
+      for (int j = j0; j < j1; ++j) {
+        const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+        const NetDev& net = F.net[j];
+        double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        if constexpr (!Op::kRaw) {
+          if (valid) row_u(F, j, pos, az, pol, u);
+        }
+        // ---- input encoding -> A columns [sub*k0/2, (sub+1)*k0/2)
+        {
+          const int k0 = P->k0, half = k0 >> 1;
+          for (int c = sub * half; c < (sub + 1) * half; c += 8) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int k = c + e;
+              float x = 0.f;
+              if (valid) {
+                if constexpr (Op::kRaw) {
+                  x = (float)op.raw(slot, k);
+                } else if (k < 5) {
+                  x = (float)u[k];
+                } else if (net.encoding == ENC_PE6 && k < 5 + 10 * DDF_PE_OCTAVES) {
+                  const int o = (k - 5) / 10, rr = (k - 5) % 10;
+                  float sv, cv;
+                  sincospif(ldexpf((float)u[rr % 5], o), &sv, &cv);
+                  x = rr < 5 ? sv : cv;
+                }
+              }
+              v[e] = x;
+            }
+            st_shared_v4(a_base + a_off(r, c), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                         pack_bf16(v[6], v[7]));
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) { mbar_arrive(BAR_A_READY(0)); mbar_arrive(BAR_A_READY(1)); }
+
+        const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
+        float head_part = 0.f;
+        for (int s = 0; s < ns; ++s) {
+          const Step& st = Op::kGrad ? P->grad[s] : P->fwd[s];
+          const int epi = st.epi;
+          const bool wa = writes_a(epi);
+          for (int h = 0; h < st.nh; ++h) {
+            mbar_wait(BAR_ACC(h), acc_ph[h] & 1u);
+            ++acc_ph[h];
+            tc_after_sync();
+            if (wa) { mbar_wait(BAR_A_FREE(h), free_ph[h] & 1u); ++free_ph[h]; }
+            const int col0 = h * st.rows;
+            if (epi == E_BWD_OUT) {
+              if (sub == 0) {
+                // d pred / d inputs for this row: st.rows (= k0) fp32 columns
+                float g[128];
+                for (int c = 0; c < st.rows; c += 16) {
+                  uint32_t rg[16];
+                  DDF_TMEM_LD16(tmem + lane_addr + (uint32_t)c, rg);
+                  tmem_wait_ld();
+#pragma unroll
+                  for (int e = 0; e < 16; ++e) g[c + e] = __uint_as_float(rg[e]);
+                }
+                if constexpr (Op::kGrad) {
+                  if (valid) {
+                    if constexpr (Op::kRaw) {
+                      op.store_grad_raw(slot, [&](int k) { return (double)g[k]; });
+                    } else {
+                      double g5[5];
+                      pe_chain(net, u, [&](int k) { return (double)g[k]; }, g5);
+                      op.store_grad(slot, g5);
+                    }
+                  }
+                }
+              }
+              tc_before_sync();
+              continue;
+            }
+            for (int c = col0 + sub * 32; c < col0 + st.rows; c += 64) {
+              uint32_t rg[32];
+              DDF_TMEM_LD32(tmem + lane_addr + (uint32_t)c, rg);
+              tmem_wait_ld();
+              float v[32];
+              if (epi == E_BWD_MASK_A) {
+                const uint32_t mw = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = ((mw >> e) & 1u) ? __uint_as_float(rg[e]) : 0.f;
+              } else {
+                uint32_t mw = 0;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                  const float z = __uint_as_float(rg[e]) + __ldg(st.bias + c + e);
+                  const bool on = z > 0.f;
+                  mw |= (on ? 1u : 0u) << e;
+                  v[e] = on ? z : 0.f;
+                }
+                if (epi == E_RELU_MASK_A) my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
+                if (epi == E_MASKG_A) {
+#pragma unroll
+                  for (int e = 0; e < 32; ++e) v[e] = ((mw >> e) & 1u) ? __ldg(P->head_w + c + e) : 0.f;
+                }
+                if (epi == E_HEAD) {
+#pragma unroll
+                  for (int e = 0; e < 32; ++e) head_part = fmaf(v[e], __ldg(P->head_w + c + e), head_part);
+                }
+              }
+              if (wa) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 8)
+                  st_shared_v4(a_base + a_off(r, c + e), pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
+                               pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
+              }
+            }
+            tc_before_sync();
+            if (wa) {
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(BAR_A_READY(h));
+            }
+          }
+          if (epi == E_HEAD) {
+            S.red[sub * ROWS + r] = head_part;
+            named_sync(1, N_EPI_WARPS * 32);
+            if (sub == 0) {
+              double p = (double)(S.red[r] + S.red[ROWS + r] + P->head_b);
+              if (F.composite) p = dmul(net.scale, p);
+              if (j == j0 || p < best) { best = p; bobj = j; }
+            }
+            named_sync(1, N_EPI_WARPS * 32);
+          }
+        }
+      }
+      if constexpr (!Op::kGrad) {
+        if (sub == 0 && valid) op.store_fwd(slot, best, bobj);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------ host side
+struct NetImage {
+  void* dev = nullptr;       // Prog (device)
+  void* img = nullptr;       // fwd + grad images
+  void* params = nullptr;    // biases + head weights (fp32)
+  int in_width = 0;
+  Prog host{};
+};
+
+inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
+
+// Append the chunks of one step: B[n][k] = src(n, k), n < N (rows), k < K.
+template <class Src>
+inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src) {
+  st.img_off = (long long)img.size() * 2;
+  for (int h = 0; h < st.nh; ++h)
+    for (int kc = 0; kc < st.nchunk; ++kc) {
+      const size_t base = img.size();
+      img.resize(base + (size_t)st.rows * 64, 0);
+      for (int n = 0; n < st.rows; ++n)
+        for (int k = 0; k < 64; ++k) {
+          const int gn = h * st.rows + n, gk = kc * 64 + k;
+          const float v = (gk < st.K) ? src(gn, gk) : 0.f;
+          __nv_bfloat16 b = __float2bfloat16_rn(v);
+          const size_t off = (size_t)(n >> 3) * 512 + (size_t)(n & 7) * 64 + (size_t)((((k >> 3) ^ (n & 7)) << 3) + (k & 7));
+          std::memcpy(&img[base + off], &b, 2);
+        }
+    }
+}
+
+inline Step make_step(int K, int N, int nh, int epi) {
+  Step s{};
+  s.K = K; s.N = N; s.nh = nh; s.epi = epi;
+  s.rows = N / nh;
+  s.nchunk = (K + 63) / 64;
+  s.chunk_bytes = s.rows * 128;
+  s.mask_layer = -1;
+  s.bias = nullptr;
+  return s;
+}
+
+// Build forward and gradient programs + UMMA images for one network.
+// weights: concat of W_l (out, in) row-major float64; biases: concat of b_l.
+inline int build_image(const int32_t* widths, int32_t n_widths, const double* weights, const double* biases,
+                       NetImage* out, std::string* err) {
+  const int L = n_widths - 1;
+  out->in_width = widths[0];
+  if (L < 2) { *err = "bf16 engine needs at least one hidden layer"; return 1; }
+  std::vector<int> wp(n_widths);
+  wp[0] = pad_to(widths[0], 16);
+  for (int l = 1; l < L; ++l) wp[l] = pad_to(widths[l], 64);
+  wp[L] = 1;
+  for (int l = 1; l < L; ++l)
+    if (wp[l] > 512) { *err = "bf16 engine supports hidden widths up to 512"; return 1; }
+  if (wp[0] > 128) { *err = "bf16 engine supports input widths up to 128"; return 1; }
+  // host copies of effective weights, padded
+  std::vector<std::vector<float>> W(L), B(L);
+  size_t wo = 0, bo = 0;
+  for (int l = 0; l < L; ++l) {
+    const int in = widths[l], o = widths[l + 1];
+    W[l].assign((size_t)wp[l + 1] * wp[l], 0.f);
+    B[l].assign(wp[l + 1], 0.f);
+    for (int a = 0; a < o; ++a) {
+      for (int k = 0; k < in; ++k) W[l][(size_t)a * wp[l] + k] = (float)weights[wo + (size_t)a * in + k];
+      B[l][a] = (float)biases[bo + a];
+    }
+    wo += (size_t)o * in;
+    bo += o;
+  }
+  Prog& P = out->host;
+  std::memset(&P, 0, sizeof(P));
+  P.k0 = wp[0];
+  P.in_width = widths[0];
+  P.encoding = widths[0] == 65 ? ENC_PE6 : ENC_RAW5;
+  P.head_b = B[L - 1][0];
+  // fp32 params: biases of hidden layers then head weights
+  std::vector<float> params;
+  std::vector<size_t> bias_off(L);
+  for (int l = 0; l < L - 1; ++l) { bias_off[l] = params.size(); params.insert(params.end(), B[l].begin(), B[l].end()); }
+  const size_t head_off = params.size();
+  params.insert(params.end(), W[L - 1].begin(), W[L - 1].begin() + wp[L - 1]);
+
+  std::vector<uint16_t> img;
+  // forward program: hidden layers 0..L-2, the last one fused with the head
+  P.n_fwd = L - 1;
+  for (int l = 0; l < L - 1; ++l) {
+    Step s = make_step(wp[l], wp[l + 1], 2, l == L - 2 ? E_HEAD : E_RELU_A);
+    const std::vector<float>& w = W[l];
+    const int K = wp[l];
+    append_chunks(img, s, [&](int n, int k) { return w[(size_t)n * K + k]; });
+    s.bias = reinterpret_cast<const float*>(bias_off[l]);   // patched to device below
+    P.fwd[l] = s;
+  }
+  const size_t fwd_bytes = img.size() * 2;
+  std::vector<uint16_t> gimg;
+  int gs = 0;
+  for (int l = 0; l < L - 1; ++l) {
+    Step s = make_step(wp[l], wp[l + 1], 2, l == L - 2 ? E_MASKG_A : E_RELU_MASK_A);
+    s.mask_layer = l;
+    const std::vector<float>& w = W[l];
+    const int K = wp[l];
+    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)n * K + k]; });
+    s.bias = reinterpret_cast<const float*>(bias_off[l]);
+    P.grad[gs++] = s;
+  }
+  // backward: layer l maps d z_l (width wp[l+1]) to d h_l (width wp[l]) with B[n][k] = W_l[k][n]
+  for (int l = L - 2; l >= 0; --l) {
+    const bool last = l == 0;
+    Step s = make_step(wp[l + 1], wp[l], last ? 1 : 2, last ? E_BWD_OUT : E_BWD_MASK_A);
+    s.mask_layer = l - 1;
+    const std::vector<float>& w = W[l];
+    const int Kin = wp[l];
+    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)k * Kin + n]; });
+    P.grad[gs++] = s;
+  }
+  P.n_grad = gs;
+  if (gs > 2 * DDF_MAX_LAYERS) { *err = "too many layers"; return 1; }
+  P.kmax = 0;
+  P.max_chunk_bytes = 0;
+  for (int i = 0; i < P.n_fwd; ++i) { P.kmax = std::max(P.kmax, std::max(P.fwd[i].K, P.fwd[i].N)); P.max_chunk_bytes = std::max(P.max_chunk_bytes, P.fwd[i].chunk_bytes); }
+  for (int i = 0; i < P.n_grad; ++i) { P.kmax = std::max(P.kmax, std::max(P.grad[i].K, P.grad[i].N)); P.max_chunk_bytes = std::max(P.max_chunk_bytes, P.grad[i].chunk_bytes); }
+  // upload
+  const size_t total = fwd_bytes + gimg.size() * 2;
+  if (cudaMalloc(&out->img, total) != cudaSuccess) { *err = "cudaMalloc (weight image) failed"; return 4; }
+  cudaMemcpy(out->img, img.data(), fwd_bytes, cudaMemcpyHostToDevice);
+  cudaMemcpy((uint8_t*)out->img + fwd_bytes, gimg.data(), gimg.size() * 2, cudaMemcpyHostToDevice);
+  if (cudaMalloc(&out->params, params.size() * 4) != cudaSuccess) { *err = "cudaMalloc (params) failed"; return 4; }
+  cudaMemcpy(out->params, params.data(), params.size() * 4, cudaMemcpyHostToDevice);
+  const float* pdev = reinterpret_cast<const float*>(out->params);
+  for (int i = 0; i < P.n_fwd; ++i) P.fwd[i].bias = pdev + (size_t)P.fwd[i].bias;
+  for (int i = 0; i < P.n_grad; ++i) P.grad[i].bias = P.grad[i].bias ? pdev + (size_t)P.grad[i].bias : nullptr;
+  // forward step 0's bias offset is 0 -> nullptr check above would drop it for grad step 0; fix explicitly
+  P.grad[0].bias = pdev + bias_off[0];
+  P.head_w = pdev + head_off;
+  P.img_fwd = reinterpret_cast<const uint8_t*>(out->img);
+  P.img_grad = reinterpret_cast<const uint8_t*>(out->img) + fwd_bytes;
+  if (cudaMalloc(&out->dev, sizeof(Prog)) != cudaSuccess) { *err = "cudaMalloc (program) failed"; return 4; }
+  if (cudaMemcpy(out->dev, &P, sizeof(Prog), cudaMemcpyHostToDevice) != cudaSuccess) { *err = "upload failed"; return 4; }
   return 0;
 }
-inline void free_image(NetImage* img) { if (img->dev) cudaFree(img->dev); img->dev = nullptr; }
-template <class Op>
-int launch(const FieldDev&, const Op&, int, bool, int, cudaStream_t, std::string* err) {
-  *err = "bf16 tcgen05 engine not built yet";
-  return 1;
+
+inline void free_image(NetImage* im) {
+  if (im->dev) cudaFree(im->dev);
+  if (im->img) cudaFree(im->img);
+  if (im->params) cudaFree(im->params);
+  im->dev = im->img = im->params = nullptr;
 }
+
+constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in per CTA
+
+template <class Op>
+int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
+           uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
+  int kmax = 0, chunk = 0;
+  for (int j = 0; j < F.n_obj; ++j) {
+    kmax = std::max(kmax, images[j].host.kmax);
+    chunk = std::max(chunk, images[j].host.max_chunk_bytes);
+  }
+  const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
+  const int extra = 1024 /*align*/ + 8 * (6 + 2 * 8) + 16 + 2 * ROWS * 4;
+  int n_stages = (SMEM_LIMIT - a_bytes - extra) / chunk;
+  n_stages = std::min(n_stages, 8);
+  if (n_stages < 2) { *err = "bf16 engine: not enough shared memory for the weight pipeline"; return 1; }
+  const size_t smem = (size_t)a_bytes + (size_t)n_stages * chunk + extra;
+  auto kern = mlp_kernel<Op>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
+  const int tiles_max = (max_rows + ROWS - 1) / ROWS + (Op::kGrad ? F.n_obj : 0);
+  const int grid = std::max(1, std::min(tiles_max, sm_count));
+  kern<<<grid, NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { *err = std::string("mlp_kernel launch: ") + cudaGetErrorString(e); return 4; }
+  return 0;
+}
+
 }  // namespace umma
 }  // namespace ddf
