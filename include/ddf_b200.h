@@ -128,6 +128,10 @@ int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64
    non-zero uint8 flags into list (device), count written to *count (device int32). */
 int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, void* stream);
 
+/* Diagnostics: tcgen05 engine pipeline wait-cycle counters, collected when
+   the environment variable DDF_DEBUG_UMMA has bit 1 set (16 u64 values). */
+int ddf_debug_counters(uint64_t* out16, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

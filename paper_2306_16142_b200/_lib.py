@@ -29,7 +29,8 @@ ENC_RAW5, ENC_PE6 = 0, 1
 
 EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "ddf_field_set_precision",
            "ddf_last_error", "ddf_mlp_forward", "ddf_mlp_input_grad", "ddf_query", "ddf_trace",
-           "ddf_normal", "ddf_render_path", "ddf_rng_doubles", "ddf_compact")
+           "ddf_normal", "ddf_render_path", "ddf_rng_doubles", "ddf_compact",
+           "ddf_debug_counters")
 
 
 def build(verbose: bool = False, force: bool = False) -> str:
@@ -106,6 +107,7 @@ def lib():
                                   ctypes.POINTER(RenderStats_t), vp]
     L.ddf_rng_doubles.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64), dp, i64, dp, vp]
     L.ddf_compact.argtypes = [dp, i64, dp, dp, vp]
+    L.ddf_debug_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), i32]
     for name in EXPORTS:
         if name != "ddf_last_error":
             getattr(L, name).restype = ctypes.c_int

@@ -679,6 +679,17 @@ int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64
   return DDF_OK;
 }
 
+int ddf_debug_counters(uint64_t* out16, int32_t reset) {
+  unsigned long long h[16];
+  CUDA_TRY(cudaMemcpyFromSymbol(h, umma::g_dbg, sizeof(h)));
+  for (int i = 0; i < 16; ++i) out16[i] = h[i];
+  if (reset) {
+    std::memset(h, 0, sizeof(h));
+    CUDA_TRY(cudaMemcpyToSymbol(umma::g_dbg, h, sizeof(h)));
+  }
+  return DDF_OK;
+}
+
 int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, void* stream) {
   if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad count");
   cudaStream_t st = (cudaStream_t)stream;

@@ -23,6 +23,7 @@
 // seed d/dh of the last hidden layer with w_head * mask, then run the
 // backward chain d_h <- (d_h * mask) @ W on the tensor cores with W^T images.
 #pragma once
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -36,6 +37,14 @@ namespace ddf {
 namespace umma {
 
 constexpr int ROWS = 128;
+// Pipeline wait-cycle counters (diagnostics): compiled in with -DDDF_PIPE_STATS=1
+#ifndef DDF_PIPE_STATS
+#define DDF_PIPE_STATS 0
+#endif
+constexpr bool kStats = DDF_PIPE_STATS != 0;
+__device__ unsigned long long g_dbg[16];
+#define DDF_DBG_T0() long long _t0 = kStats ? clock64() : 0
+#define DDF_DBG_ADD(i) do { if (kStats) atomicAdd(&g_dbg[i], (unsigned long long)(clock64() - _t0)); } while (0)
 constexpr int NTHREADS = 320;
 constexpr int EPI_WARP0 = 2;
 constexpr int N_EPI_WARPS = 8;
@@ -44,7 +53,7 @@ constexpr int MASK_WORDS_PER_CTA = DDF_MAX_LAYERS * 16 * ROWS;   // u32: [layer]
 enum Epi : int { E_RELU_A = 0, E_HEAD = 1, E_RELU_MASK_A = 2, E_MASKG_A = 3, E_BWD_MASK_A = 4, E_BWD_OUT = 5 };
 __host__ __device__ inline bool writes_a(int e) { return e == E_RELU_A || e == E_RELU_MASK_A || e == E_MASKG_A || e == E_BWD_MASK_A; }
 
-struct Step {
+struct __align__(16) Step {
   int K, N, nh, epi;
   int nchunk;          // 64-wide K chunks per half
   int rows;            // N / nh (MMA N)
@@ -53,6 +62,21 @@ struct Step {
   long long img_off;   // byte offset of the step's first chunk in the image
   const float* bias;   // fp32 (N) or nullptr
 };
+static_assert(sizeof(Step) == 48, "Step is loaded as three 16-byte vectors");
+
+// One step descriptor -> registers with three independent 16-byte loads (the
+// roles would otherwise re-read fields after every barrier asm, and with
+// 227 KB of shared memory carved out those loads miss L1).
+__device__ __forceinline__ Step load_step(const Step* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  Step s;
+  s.K = a.x; s.N = a.y; s.nh = a.z; s.epi = a.w;
+  s.nchunk = b.x; s.rows = b.y; s.chunk_bytes = b.z; s.mask_layer = b.w;
+  s.img_off = (long long)(((unsigned long long)(unsigned)c.y << 32) | (unsigned)c.x);
+  s.bias = reinterpret_cast<const float*>(((unsigned long long)(unsigned)c.w << 32) | (unsigned)c.z);
+  return s;
+}
 
 struct Prog {
   int n_fwd, n_grad;
@@ -156,6 +180,119 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// One epilogue half for one warp: its NM 32-column chunks of the accumulator
+// -> registers -> (bias, ReLU, masks, head dot) -> packed bf16 -> A tile.  The
+// first two packed chunks are held until the A columns are free (a_free),
+// later chunks store directly.  Specialised per epilogue kind and chunk count
+// so each fully unrolled loop carries only the arithmetic it needs.
+template <int EPI, int NM>
+__device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
+                                           uint32_t* my_masks, const float* head_w, float& head_part,
+                                           uint32_t bar_free, uint32_t& free_ph) {
+  constexpr bool WA = EPI == E_RELU_A || EPI == E_RELU_MASK_A || EPI == E_MASKG_A || EPI == E_BWD_MASK_A;
+  constexpr bool BIAS = EPI != E_BWD_MASK_A;
+  constexpr int HOLD = NM < 2 ? NM : 2;
+  const int r7 = r & 7;
+  uint32_t hold[HOLD > 0 ? HOLD : 1][16];
+  auto store = [&](int c, const uint32_t* pk) {
+    // 4 x 16 B of one row into the 128B-swizzled A tile (row base a_row)
+    const uint32_t blk = a_row + (uint32_t)((c >> 6) * (ROWS * 128));
+    const int cc0 = (c & 63) >> 3;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      st_shared_v4(blk + (uint32_t)(((cc0 + e) ^ r7) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+  };
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const int c = c_first + i * 64;
+    uint32_t rg[32];
+    DDF_TMEM_LD32(tmem_row + (uint32_t)c, rg);
+    // this chunk's operands load while the TMEM read is in flight
+    float4 bq[8];
+    uint32_t mq = 0u;
+    if constexpr (BIAS) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) bq[k] = __ldg(reinterpret_cast<const float4*>(st.bias + c) + k);
+    } else {
+      mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
+    }
+    tmem_wait_ld();
+    const float* bf = reinterpret_cast<const float*>(bq);
+    uint32_t pkd[16];
+    if constexpr (EPI == E_BWD_MASK_A) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pkd[e] = pack_bf16(((mq >> (2 * e)) & 1u) ? __uint_as_float(rg[2 * e]) : 0.f,
+                           ((mq >> (2 * e + 1)) & 1u) ? __uint_as_float(rg[2 * e + 1]) : 0.f);
+    } else if constexpr (EPI == E_RELU_A) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pkd[e] = pack_bf16(fmaxf(__uint_as_float(rg[2 * e]) + bf[2 * e], 0.f),
+                           fmaxf(__uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1], 0.f));
+    } else if constexpr (EPI == E_HEAD) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w + c + e));
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+      }
+    } else {
+      // ReLU mask bits of this row's 32 columns (neural.py:241 "h > 0")
+      uint32_t mw = 0u;
+      float v[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float z = __uint_as_float(rg[e]) + bf[e];
+        mw |= (z > 0.f ? 1u : 0u) << e;
+        v[e] = fmaxf(z, 0.f);
+      }
+      if constexpr (EPI == E_RELU_MASK_A) {
+        my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
+      } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w + c + e));
+          v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
+          v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
+          v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
+          v[e + 3] = ((mw >> (e + 3)) & 1u) ? hw.w : 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+    }
+    if constexpr (WA) {
+      if (i < HOLD) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) hold[i][e] = pkd[e];
+      }
+      if (i == HOLD - 1) {
+        mbar_wait(bar_free, free_ph & 1u);
+        ++free_ph;
+#pragma unroll
+        for (int q2 = 0; q2 < HOLD; ++q2) store(c_first + q2 * 64, hold[q2]);
+      } else if (i >= HOLD) {
+        store(c, pkd);
+      }
+    }
+  }
+  if constexpr (WA && NM == 0) ++free_ph;   // no columns in this half: keep the phase count in step
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_half(int nmine, const Step& st, int c_first, int r, uint32_t tmem_row,
+                                         uint32_t a_row, uint32_t* my_masks, const float* head_w, float& head_part,
+                                         uint32_t bar_free, uint32_t& free_ph) {
+  switch (nmine) {
+    case 0: epi_chunks<EPI, 0>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
+    case 1: epi_chunks<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
+    case 2: epi_chunks<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
+    default: epi_chunks<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
+  }
+}
+
 // ------------------------------------------------------------------ tiles
 // Forward: tile t covers list rows [128 t, 128 t + 128) and runs every object.
 // Gradient: tiles enumerate (object, 128-row block) over the object segments.
@@ -202,13 +339,13 @@ struct Smem {
 template <class Op>
 __global__ void __launch_bounds__(NTHREADS, 1)
 mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int a_bytes,
-           int stage_bytes) {
+           int stage_bytes, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem S;
   S.a = base_ptr;
   S.stages = base_ptr + a_bytes;
-  S.bars = reinterpret_cast<uint64_t*>(S.stages + (size_t)n_stages * stage_bytes);
+  S.bars = reinterpret_cast<uint64_t*>(S.stages + (size_t)((dbg & 8) ? 1 : n_stages) * stage_bytes);
   S.tmem_slot = reinterpret_cast<uint32_t*>(S.bars + 6 + 2 * n_stages);
   S.red = reinterpret_cast<float*>(S.tmem_slot + 4);
 
@@ -243,6 +380,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
   const uint32_t a_base = smem_u32(S.a);
   const uint32_t st_base = smem_u32(S.stages);
   const int tiles = n_tiles(F, op);
+  const int sstride = (dbg & 8) ? 0 : stage_bytes;   // dbg 8: all stages alias one buffer (timing only)
 
   if (warp == 0) {
     // ================================================= weight producer
@@ -254,16 +392,24 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
         tile_rows(F, op, t, j0, j1, base, nv);
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
-          const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
+          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
           const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
           for (int s = 0; s < ns; ++s) {
-            const Step& st = Op::kGrad ? P->grad[s] : P->fwd[s];
+            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
             const uint8_t* src = img + st.img_off;
             const int nck = st.nh * st.nchunk;
             for (int c = 0; c < nck; ++c) {
-              mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
-              mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
-              bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+              {
+                DDF_DBG_T0();
+                mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
+                DDF_DBG_ADD(6);
+              }
+              if (dbg & 1) {   // timing experiment only: no weight traffic (wrong results)
+                mbar_arrive(BAR_FULL(stage));
+              } else {
+                mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
+                bulk_g2s(st_base + (uint32_t)(stage * sstride), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+              }
               src += st.chunk_bytes;
               if (++stage == n_stages) { stage = 0; phase ^= 1u; }
             }
@@ -274,6 +420,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
   } else if (warp == 1) {
     // ================================================= MMA issuer
     if (lane == 0) {
+      DDF_DBG_T0();
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ar[2] = {0u, 0u};
@@ -285,7 +432,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
           const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
           int prev_rows = 1 << 30;
           for (int s = 0; s < ns; ++s) {
-            const Step& st = Op::kGrad ? P->grad[s] : P->fwd[s];
+            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
             const uint32_t id = idesc(st.rows);
             const bool wa = writes_a(st.epi);
             const int c0 = min(st.nchunk - 1, ((st.N >> 1) - 1) >> 6);   // last chunk touching A cols < N/2
@@ -300,13 +447,22 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
             for (int h = 0; h < st.nh; ++h) {
               for (int kc = 0; kc < st.nchunk; ++kc) {
                 const bool need1 = (kc * 64 + 63) >= (st.K >> 1);
-                if (!waited0) { mbar_wait(BAR_A_READY(0), ar[0] & 1u); ++ar[0]; waited0 = true; }
-                if (need1 && !waited1) { mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; waited1 = true; }
-                mbar_wait(BAR_FULL(stage), phase);
+                {
+                  DDF_DBG_T0();
+                  if (!waited0) { mbar_wait(BAR_A_READY(0), ar[0] & 1u); ++ar[0]; waited0 = true; }
+                  if (need1 && !waited1) { mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; waited1 = true; }
+                  DDF_DBG_ADD(0);
+                }
+                {
+                  DDF_DBG_T0();
+                  mbar_wait(BAR_FULL(stage), phase);
+                  DDF_DBG_ADD(1);
+                }
                 tc_after_sync();
+                const long long t_is = kStats ? clock64() : 0;
                 const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
                 const uint32_t a_chunk = a_base + (uint32_t)(kc * ROWS * 128);
-                const uint32_t b_chunk = st_base + (uint32_t)(stage * stage_bytes);
+                const uint32_t b_chunk = st_base + (uint32_t)(stage * sstride);
                 for (int ks = 0; ks < nks; ++ks) {
                   mma_bf16(tmem + (uint32_t)(h * st.rows), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
                            (kc | ks) ? 1u : 0u);
@@ -316,14 +472,17 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                   if (kc == c0) tc_commit(BAR_A_FREE(0));
                   if (kc == st.nchunk - 1) tc_commit(BAR_A_FREE(1));
                 }
+                if (kStats) atomicAdd(&g_dbg[8], (unsigned long long)(clock64() - t_is));
                 if (++stage == n_stages) { stage = 0; phase ^= 1u; }
               }
               tc_commit(BAR_ACC(h));
             }
+            if (kStats) atomicAdd(&g_dbg[5], 1ull);
             if (!waited1) { mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; }   // keep phases in step
           }
         }
       }
+      DDF_DBG_ADD(4);
     }
   } else {
     // ================================================= row warps (encoding + epilogues)
@@ -331,6 +490,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
     const int sub = (warp - EPI_WARP0) >> 2;   // column split between the two warps of a quarter
     const int r = q * 32 + lane;         // tile row == TMEM lane
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t a_row = a_base + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);   // this row in every A k-block
     uint32_t* my_masks = mask_scratch + (size_t)blockIdx.x * MASK_WORDS_PER_CTA;
     uint32_t acc_ph[2] = {0u, 0u}, free_ph[2] = {0u, 0u};
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -386,15 +546,19 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
         const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
         float head_part = 0.f;
         for (int s = 0; s < ns; ++s) {
-          const Step& st = Op::kGrad ? P->grad[s] : P->fwd[s];
+          const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
           const int epi = st.epi;
           const bool wa = writes_a(epi);
           for (int h = 0; h < st.nh; ++h) {
-            mbar_wait(BAR_ACC(h), acc_ph[h] & 1u);
+            const int col0 = h * st.rows;
+            const int c_first = col0 + sub * 32;
+            {
+              DDF_DBG_T0();
+              mbar_wait(BAR_ACC(h), acc_ph[h] & 1u);
+              if (threadIdx.x == EPI_WARP0 * 32) DDF_DBG_ADD(2);
+            }
             ++acc_ph[h];
             tc_after_sync();
-            if (wa) { mbar_wait(BAR_A_FREE(h), free_ph[h] & 1u); ++free_ph[h]; }
-            const int col0 = h * st.rows;
             if (epi == E_BWD_OUT) {
               if (sub == 0) {
                 // d pred / d inputs for this row: st.rows (= k0) fp32 columns
@@ -421,41 +585,28 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
               tc_before_sync();
               continue;
             }
-            for (int c = col0 + sub * 32; c < col0 + st.rows; c += 64) {
-              uint32_t rg[32];
-              DDF_TMEM_LD32(tmem + lane_addr + (uint32_t)c, rg);
-              tmem_wait_ld();
-              float v[32];
-              if (epi == E_BWD_MASK_A) {
-                const uint32_t mw = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) v[e] = ((mw >> e) & 1u) ? __uint_as_float(rg[e]) : 0.f;
-              } else {
-                uint32_t mw = 0;
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                  const float z = __uint_as_float(rg[e]) + __ldg(st.bias + c + e);
-                  const bool on = z > 0.f;
-                  mw |= (on ? 1u : 0u) << e;
-                  v[e] = on ? z : 0.f;
-                }
-                if (epi == E_RELU_MASK_A) my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
-                if (epi == E_MASKG_A) {
-#pragma unroll
-                  for (int e = 0; e < 32; ++e) v[e] = ((mw >> e) & 1u) ? __ldg(P->head_w + c + e) : 0.f;
-                }
-                if (epi == E_HEAD) {
-#pragma unroll
-                  for (int e = 0; e < 32; ++e) head_part = fmaf(v[e], __ldg(P->head_w + c + e), head_part);
-                }
-              }
-              if (wa) {
-#pragma unroll
-                for (int e = 0; e < 32; e += 8)
-                  st_shared_v4(a_base + a_off(r, c + e), pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
-                               pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
-              }
+            // TMEM -> registers -> epilogue math -> packed bf16, all before the A
+            // columns are free; only the shared stores wait for a_free
+            const int nmine = (st.rows - sub * 32 + 63) >> 6;   // 32-col chunks of this warp
+            const long long t_epi = kStats ? clock64() : 0;
+            switch (epi) {
+              case E_RELU_A:
+                epi_half<E_RELU_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                break;
+              case E_RELU_MASK_A:
+                epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                break;
+              case E_MASKG_A:
+                epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                break;
+              case E_BWD_MASK_A:
+                epi_half<E_BWD_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                break;
+              default:
+                epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                break;
             }
+            if (kStats && threadIdx.x == EPI_WARP0 * 32) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - t_epi));
             tc_before_sync();
             if (wa) {
               fence_async_smem();
@@ -647,13 +798,15 @@ int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op,
   int n_stages = (SMEM_LIMIT - a_bytes - extra) / chunk;
   n_stages = std::min(n_stages, 8);
   if (n_stages < 2) { *err = "bf16 engine: not enough shared memory for the weight pipeline"; return 1; }
-  const size_t smem = (size_t)a_bytes + (size_t)n_stages * chunk + extra;
+  static const int dbg = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
+  if (dbg & 8) n_stages = 8;
+  const size_t smem = (size_t)a_bytes + (size_t)((dbg & 8) ? 1 : n_stages) * chunk + extra;
   auto kern = mlp_kernel<Op>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
   const int tiles_max = (max_rows + ROWS - 1) / ROWS + (Op::kGrad ? F.n_obj : 0);
   const int grid = std::max(1, std::min(tiles_max, sm_count));
-  kern<<<grid, NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk);
+  kern<<<grid, NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, dbg);
   e = cudaGetLastError();
   if (e != cudaSuccess) { *err = std::string("mlp_kernel launch: ") + cudaGetErrorString(e); return 4; }
   return 0;
