@@ -519,9 +519,9 @@ class PathConfig:
     rr_start: int = -1          # EXTENSION: Russian roulette from this bounce index (-1 = off)
 
 
-def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None):
+def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None, pixels=None):
     """render.py:198-247 over the contiguous global pixel range ``pix_range``
-    (default: the whole film).  Random draws are addressed by global index so
+    or the ascending pixel subset ``pixels`` (default: the whole film).  Random draws are addressed by global index so
     any range reproduces the full-frame stream.  Returns the (P,) grey value
     per pixel of the range (accum / spp, film summed in spp order).
 
@@ -532,13 +532,23 @@ def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None)
     if cfg.bounces < 1:
         raise ValueError("path mode needs bounces >= 1")
     n_pix = cam.width * cam.height
-    i0, i1 = (0, n_pix) if pix_range is None else pix_range
-    pix = np.arange(i0, i1)
+    if pixels is not None:            # any ascending subset (e.g. one rank's tiles)
+        pix = np.asarray(pixels, dtype=np.int64)
+        i0, i1 = (int(pix.min()), int(pix.max()) + 1) if len(pix) else (0, 0)
+    else:
+        i0, i1 = (0, n_pix) if pix_range is None else pix_range
+        pix = np.arange(i0, i1)
     P = len(pix)
+    sel = pix - i0
+
+    def block(tag, k0, per):
+        """`per` draws per pixel for pixels i0..i1-1 from draw index k0, rows of pix."""
+        b = stream_block(cfg.seed, tag, k0 + per * i0, per * (i1 - i0)).reshape(i1 - i0, per)
+        return b[sel]
     accum = np.zeros(P)
     alb = None if fld.albedos is None else np.asarray(fld.albedos, dtype=np.float64)
     for s in range(cfg.spp):
-        jit = stream_block(cfg.seed, RNG_TAG, draw_index(s, 0, n_pix, cfg.bounces) + 2 * i0, 2 * P).reshape(P, 2)
+        jit = block(RNG_TAG, draw_index(s, 0, n_pix, cfg.bounces), 2)
         o, d = camera_rays(cam, jit, pix)
         rad = np.zeros(P)
         thr = np.ones(P)
@@ -549,9 +559,9 @@ def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None)
         pos = o
         stages = []
         for b in range(cfg.bounces):
-            u = stream_block(cfg.seed, RNG_TAG, draw_index(s, 1 + b, n_pix, cfg.bounces) + 2 * i0, 2 * P).reshape(P, 2)
+            u = block(RNG_TAG, draw_index(s, 1 + b, n_pix, cfg.bounces), 2)
             if cfg.rr_start >= 0 and b >= cfg.rr_start and alive.any():
-                rr = stream_block(cfg.seed, RR_TAG, (s * cfg.bounces + b) * n_pix + i0, P)
+                rr = block(RR_TAG, (s * cfg.bounces + b) * n_pix, 1)[:, 0]
                 idx = np.nonzero(alive)[0]
                 p = np.minimum(1.0, thr[idx])
                 live = rr[idx] < p

@@ -43,9 +43,29 @@ def test_no_device_fails_loudly():
     assert b"no CUDA device" in _lib.lib().ddf_last_error()
 
 
-def test_struct_layouts_match_header():
-    assert ctypes.sizeof(_lib.Camera_t) == 8 * 14 + 8
-    assert ctypes.sizeof(_lib.RenderStats_t) == 40
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors == the C header's struct sizes and field offsets (gcc)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    src = tmp_path / "sz.c"
+    fields = {"ddf_camera_t": _lib.Camera_t, "ddf_path_config_t": _lib.PathConfig_t,
+              "ddf_render_stats_t": _lib.RenderStats_t}
+    body = []
+    for cname, py in fields.items():
+        body.append(f'printf("%zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            body.append(f'printf("%zu\\n", offsetof({cname}, {fname}));')
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ddf_b200.h"\nint main(){' + "".join(body) + "return 0;}")
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.dirname(_lib.HEADER), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = []
+    for py in fields.values():
+        want.append(ctypes.sizeof(py))
+        want += [getattr(py, f).offset for f, _ in py._fields_]
+    assert got == want
 
 
 def test_ddfn_roundtrip_matches_reference_bytes(golden):
