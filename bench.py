@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
@@ -111,6 +111,103 @@ def cpu_baseline(name, runs=1):
             "sample": desc + "; float64 numpy oracle (oracle/cpu_ddf.py), OpenBLAS threads"}
 
 
+# ----------------------------------------------------------------- config 1: query batch
+def cpu_queries(args, reference_line=False):
+    """Config 1 on the CPU: NeuralField.query_batch of the oracle (f64) on the
+    full 65,536-ray batch, all OpenBLAS threads."""
+    from oracle import cpu_ddf as O
+    from paper_2306_16142_b200 import configs as C
+    w = C.WORKLOADS["c1"]
+    m = C.models("c1")[0]
+    f = O.Field([O.Net(m.widths, m.v, m.g, m.b)], C.CFG_DELTA, bounds=C.UNIT_BOX)
+    o, d = C.query_rays(w["n"], 0)
+    f.query(o, d)
+    reps = max(1, args.steps) if reference_line else 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        f.query(o, d)
+    s = (time.perf_counter() - t0) / reps
+    v = w["n"] / s
+    base = {"value": v, "unit": "queries/s", "cores": cpu_cores(), "kind": "port",
+            "sample": "full 65,536-ray batch, oracle query (field.py:248-258 restated), float64"}
+    if not reference_line:
+        return base
+    return {"impl": "reference", "metric": "ddf_queries_per_s", "value": v, "unit": "queries/s", "n_gpus": args.gpus,
+            "steps": reps, "warmup": 1, "ms_per_step": 1e3 * s, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": "c1", "n": w["n"]},
+            "cpu_baseline": base, "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}
+
+
+def bench_queries(args, rank, world, local):
+    """Config 1: one step = NeuralField.query_batch of 65,536 rays (5->4x128->1,
+    fp32) through ddf_query, inputs resident on the device (value) and from
+    pinned host arrays with results read back (e2e)."""
+    import ctypes
+
+    import torch
+    from paper_2306_16142_b200 import _lib
+    from paper_2306_16142_b200 import configs as C
+    w = C.WORKLOADS["c1"]
+    prec = args.precision or w["precision"]
+    f = C.build_field("c1", precision=prec)
+    o, d = C.query_rays(w["n"], 0)
+    n = w["n"]
+    od, dd = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    t = torch.empty(n, dtype=torch.float64, device="cuda")
+    pred = torch.empty(n, dtype=torch.float64, device="cuda")
+    hit = torch.empty(n, dtype=torch.uint8, device="cuda")
+    L = _lib.lib()
+    st = torch.cuda.current_stream()
+    P = lambda x: ctypes.c_void_p(x.data_ptr())  # noqa: E731
+
+    def step():
+        _lib.check(L.ddf_query(f.handle, P(od), P(dd), n, P(t), P(hit), P(pred), None,
+                               ctypes.c_void_p(st.cuda_stream)))
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            step()
+            e1.record(st)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.mean(times))
+    # e2e through the public protocol call (numpy in, numpy out)
+    f.query_raw(o, d)
+    te = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        f.query_raw(o, d)
+        te.append(time.perf_counter() - t0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    F = C.mlp_flops(w["widths"])
+    ach = F * n / (ms / 1e3) / 1e12
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    out = {"metric": "ddf_queries_per_s", "value": n / (ms / 1e3), "unit": "queries/s", "n_gpus": world,
+           "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+           "config": {"workload": "c1", "n": n, "widths": list(w["widths"]), "precision": prec,
+                      "l2": "flushed (256 MB write) between timed steps"},
+           "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                        "traffic": None, "kernel": "fused DDF-MLP query (launch-latency bound at 65,536 rows)"},
+           "cpu_baseline": cpu_queries(args),
+           "e2e": {"value": n / float(np.mean(te)), "unit": "queries/s", "h2d_bytes_per_step": 2 * n * 24,
+                   "d2h_bytes_per_step": n * (8 + 8 + 1 + 4)},
+           "gpu_launches": args.steps, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(out))
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -167,6 +264,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     name = args.config
 
+    if args.impl == "reference" and name == "c1":
+        if rank != 0:
+            return
+        print(json.dumps(cpu_queries(args, reference_line=True)))
+        return
     if args.impl == "reference":
         if rank != 0:
             return
@@ -197,6 +299,9 @@ def main():
     import torch.distributed as dist
     from paper_2306_16142_b200 import configs as C
     from paper_2306_16142_b200 import render as R
+
+    if name == "c1":
+        return bench_queries(args, rank, world, local)
 
     torch.cuda.set_device(local)
     if world > 1:
