@@ -1,0 +1,121 @@
+"""Edge cases on the GPU path: empty and single-row batches,
+axis-aligned directions (zero components: the slab test's special branch,
+field.py:332-336), rays starting inside the box, tiny films, odd tilings,
+bounces = 1, Russian roulette from bounce 0, and the error classes."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import cpu_ddf as O  # noqa: E402
+from paper_2306_16142_b200 import render as R  # noqa: E402
+from paper_2306_16142_b200.dist import owned_pixels  # noqa: E402
+from paper_2306_16142_b200.errors import DataError  # noqa: E402
+from paper_2306_16142_b200.field import CudaNeuralField  # noqa: E402
+from paper_2306_16142_b200.neural import kaiming_uniform, save_model  # noqa: E402
+
+BOX = np.array([[-1.0] * 3, [1.0] * 3])
+D = 10.0 / 0.98
+
+
+@pytest.fixture(scope="module")
+def pair():
+    m = kaiming_uniform((5, 64, 64, 64, 1), 12)
+    return m, CudaNeuralField(m, D, bounds=BOX), O.Field([O.Net(m.widths, m.v, m.g, m.b)], D, bounds=BOX)
+
+
+def test_empty_batches(pair):
+    _, f, _ = pair
+    e = np.zeros((0, 3))
+    t, h = f.trace_batch(e, e)
+    assert t.shape == (0,) and h.shape == (0,)
+    t, h = f.query_batch(e, e)
+    assert t.shape == (0,)
+    n, v = f.normal_batch(e, e)
+    assert n.shape == (0, 3)
+    assert f.forward_inputs(np.zeros((0, 5))).shape == (0,)
+
+
+def test_single_row_and_axis_aligned_rays(pair):
+    _, f, of = pair
+    o = np.array([[0.0, 0.0, 3.0], [0.5, -0.2, 3.0], [2.0, 0.0, 0.0], [0.0, 1.0, 0.5], [0.3, 0.3, 0.3],
+                  [1.5, 1.5, 0.0], [1.0, 0.2, 0.1]])
+    d = np.array([[0.0, 0.0, -1.0], [0.0, 0.0, -1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0], [0.0, 1.0, 0.0],
+                  [0.0, 0.0, 1.0], [1.0, 0.0, 0.0]])
+    t, h = f.trace_batch(o, d)
+    tr, hr, _ = of.trace(o, d)
+    assert np.array_equal(h, hr)
+    assert np.allclose(t[h], tr[hr], atol=1e-4)
+    t1, h1 = f.trace_batch(o[:1], d[:1])
+    assert h1[0] == h[0] and (not h[0] or abs(t1[0] - t[0]) < 1e-12)
+
+
+def test_rays_starting_inside_box(pair):
+    _, f, of = pair
+    rng = np.random.default_rng(3)
+    o = rng.uniform(-0.9, 0.9, (500, 3))
+    d = rng.normal(size=(500, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    t, h = f.trace_batch(o, d)
+    tr, hr, _ = of.trace(o, d)
+    assert (h == hr).mean() >= 0.999
+    both = h & hr
+    assert np.max(np.abs(t[both] - tr[both])) <= 1e-4
+    n, v = f.normal_batch(o, d)           # t_hit=None: gradient at the origin
+    nr, vr = of.normal(o, d)
+    assert np.degrees(np.arccos(np.clip(np.einsum("ij,ij->i", n, nr), -1, 1))).max() < 0.05
+
+
+@pytest.mark.parametrize("w,h,spp,b", [(1, 1, 1, 1), (3, 5, 2, 1), (17, 1, 3, 2), (1, 9, 1, 4)])
+def test_tiny_films(pair, w, h, spp, b):
+    m, f, of = pair
+    cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=w, height=h)
+    img = R.render_path(f, cam, R.RenderConfig(spp=spp, bounces=b, seed=4)).data[:, :, 0].reshape(-1)
+    oc = O.Cam((0, 0, 3.0), (0, 0, 0.0), vfov=np.pi / 4, width=w, height=h)
+    ref = O.render_path(of, oc, O.PathConfig(spp=spp, bounces=b, albedo=0.7, env=1.0, seed=4))
+    assert np.sqrt(np.mean((img - ref) ** 2)) <= 3e-3
+
+
+def test_odd_tiles_and_rr_from_zero(pair):
+    _, f, of = pair
+    cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=37, height=23)
+    full, _ = R.render_path_device(f, cam, R.RenderConfig(spp=2, bounces=3, seed=8, rr_start=0))
+    full = full.cpu().numpy()
+    acc = np.zeros_like(full)
+    for rank in range(3):
+        part, _ = R.render_path_device(f, cam, R.RenderConfig(spp=2, bounces=3, seed=8, rr_start=0, tile=7,
+                                                              rank=rank, world=3))
+        part = part.cpu().numpy()
+        mine = owned_pixels(37, 23, 7, rank, 3)
+        assert np.all(part[np.setdiff1d(np.arange(37 * 23), mine)] == 0.0)
+        acc += part
+    assert np.array_equal(acc, full)
+    oc = O.Cam((0, 0, 3.0), (0, 0, 0.0), vfov=np.pi / 4, width=37, height=23)
+    ref = O.render_path(of, oc, O.PathConfig(spp=2, bounces=3, albedo=0.7, env=1.0, seed=8, rr_start=0))
+    assert np.sqrt(np.mean((full / 2 - ref) ** 2)) <= 3e-3
+
+
+def test_from_checkpoint_and_bad_checkpoint(tmp_path, pair):
+    m, _, _ = pair
+    p = tmp_path / "m.ddfn"
+    save_model(m, D, p)
+    f = CudaNeuralField.from_checkpoint(p, bounds=BOX)
+    assert f.delta == D and f.normal_eval_backoff == 0.5 * D
+    (tmp_path / "bad.ddfn").write_bytes(b"DDFN" + b"\0" * 3)
+    with pytest.raises(DataError):
+        CudaNeuralField.from_checkpoint(tmp_path / "bad.ddfn")
+
+
+def test_reference_render_modes_run_on_the_shim(pair, reference):
+    """The reference's own render_depth / render_normal / render_shaded run on
+    CudaNeuralField unchanged (protocol drop-in)."""
+    _, f, _ = pair
+    _, _, render = reference
+    cam = render.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=16, height=12)
+    for mode in ("depth", "normal", "shaded"):
+        fb = render.render(f, cam, render.RenderConfig(mode=mode))
+        assert fb.data.shape[:2] == (12, 16)
