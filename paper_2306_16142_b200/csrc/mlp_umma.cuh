@@ -60,7 +60,7 @@ struct __align__(16) Step {
   int chunk_bytes;     // rows * 128
   int mask_layer;      // E_RELU_MASK_A: layer stored; E_BWD_MASK_A: layer applied
   long long img_off;   // byte offset of the step's first chunk in the image
-  const float* bias;   // fp32 (N) or nullptr
+  const float* bias;   // holds the float offset of the bias in Prog::params (no bias: unused)
 };
 static_assert(sizeof(Step) == 48, "Step is loaded as three 16-byte vectors");
 
@@ -87,6 +87,9 @@ struct Prog {
   int max_chunk_bytes;
   float head_b;
   const float* head_w; // fp32, padded last hidden width
+  const float* params; // fp32 block: hidden-layer biases then head weights (staged in shared memory)
+  int params_floats;   // multiple of 4
+  int head_off;        // float offset of the head weights in the block
   const uint8_t* img_fwd;
   const uint8_t* img_grad;
   Step fwd[DDF_MAX_LAYERS];
@@ -188,7 +191,7 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 template <int EPI, int NM>
 __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
                                            uint32_t* my_masks, const float* head_w, float& head_part,
-                                           uint32_t bar_free, uint32_t& free_ph) {
+                                           uint32_t bar_free, uint32_t& free_ph, const float* sparams) {
   constexpr bool WA = EPI == E_RELU_A || EPI == E_RELU_MASK_A || EPI == E_MASKG_A || EPI == E_BWD_MASK_A;
   constexpr bool BIAS = EPI != E_BWD_MASK_A;
   constexpr int HOLD = NM < 2 ? NM : 2;
@@ -212,7 +215,8 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
     uint32_t mq = 0u;
     if constexpr (BIAS) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) bq[k] = __ldg(reinterpret_cast<const float4*>(st.bias + c) + k);
+      for (int k = 0; k < 8; ++k)
+        bq[k] = *reinterpret_cast<const float4*>(sparams + (size_t)st.bias + c + 4 * k);   // shared memory
     } else {
       mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
     }
@@ -232,7 +236,7 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
     } else if constexpr (EPI == E_HEAD) {
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
-        const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w + c + e));
+        const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
         head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
         head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
         head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
@@ -253,7 +257,7 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
       } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
-          const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w + c + e));
+          const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
           v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
           v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
           v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
@@ -284,12 +288,12 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
 template <int EPI>
 __device__ __forceinline__ void epi_half(int nmine, const Step& st, int c_first, int r, uint32_t tmem_row,
                                          uint32_t a_row, uint32_t* my_masks, const float* head_w, float& head_part,
-                                         uint32_t bar_free, uint32_t& free_ph) {
+                                         uint32_t bar_free, uint32_t& free_ph, const float* sp) {
   switch (nmine) {
-    case 0: epi_chunks<EPI, 0>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
-    case 1: epi_chunks<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
-    case 2: epi_chunks<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
-    default: epi_chunks<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph); break;
+    case 0: epi_chunks<EPI, 0>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
+    case 1: epi_chunks<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
+    case 2: epi_chunks<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
+    default: epi_chunks<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
   }
 }
 
@@ -333,13 +337,14 @@ struct Smem {
   uint64_t* bars;       // [0..1] a_ready, [2..3] acc_ready, [4..5] a_free, [6..6+S) w_full, [..+S) w_empty
   uint32_t* tmem_slot;
   float* red;           // [2][128] head partial sums
+  float* params;        // current network's biases + head weights
 };
 
 // ------------------------------------------------------------------ kernel
 template <class Op>
 __global__ void __launch_bounds__(NTHREADS, 1)
 mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int a_bytes,
-           int stage_bytes, int dbg) {
+           int stage_bytes, int params_bytes, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem S;
@@ -348,6 +353,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
   S.bars = reinterpret_cast<uint64_t*>(S.stages + (size_t)((dbg & 8) ? 1 : n_stages) * stage_bytes);
   S.tmem_slot = reinterpret_cast<uint32_t*>(S.bars + 6 + 2 * n_stages);
   S.red = reinterpret_cast<float*>(S.tmem_slot + 4);
+  S.params = S.red + 2 * ROWS;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(S.bars);
@@ -463,9 +469,11 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                 const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
                 const uint32_t a_chunk = a_base + (uint32_t)(kc * ROWS * 128);
                 const uint32_t b_chunk = st_base + (uint32_t)(stage * sstride);
-                for (int ks = 0; ks < nks; ++ks) {
-                  mma_bf16(tmem + (uint32_t)(h * st.rows), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
-                           (kc | ks) ? 1u : 0u);
+                if (!(dbg & 128)) {   // dbg 128: timing experiment only, no MMAs (wrong results)
+                  for (int ks = 0; ks < nks; ++ks) {
+                    mma_bf16(tmem + (uint32_t)(h * st.rows), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
+                             (kc | ks) ? 1u : 0u);
+                  }
                 }
                 tc_commit(BAR_EMPTY(stage));
                 if (wa && h == st.nh - 1) {
@@ -508,6 +516,18 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
       for (int j = j0; j < j1; ++j) {
         const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
         const NetDev& net = F.net[j];
+        // this network's biases + head weights -> shared memory (every epilogue
+        // warp is past the previous network's last use: HEAD ends in a named
+        // barrier, gradient programs end with BWD_OUT which reads none)
+        const int head_off = __ldg(&P->head_off);
+        {
+          const int nf = __ldg(&P->params_floats);
+          const float4* src = reinterpret_cast<const float4*>(P->params);
+          float4* dst = reinterpret_cast<float4*>(S.params);
+          named_sync(1, N_EPI_WARPS * 32);
+          for (int i = threadIdx.x - EPI_WARP0 * 32; i < (nf >> 2); i += N_EPI_WARPS * 32) dst[i] = __ldg(src + i);
+          named_sync(1, N_EPI_WARPS * 32);
+        }
         double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         if constexpr (!Op::kRaw) {
           if (valid) row_u(F, j, pos, az, pol, u);
@@ -591,19 +611,19 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
             const long long t_epi = kStats ? clock64() : 0;
             switch (epi) {
               case E_RELU_A:
-                epi_half<E_RELU_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                epi_half<E_RELU_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
                 break;
               case E_RELU_MASK_A:
-                epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
                 break;
               case E_MASKG_A:
-                epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
                 break;
               case E_BWD_MASK_A:
-                epi_half<E_BWD_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                epi_half<E_BWD_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
                 break;
               default:
-                epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, P->head_w, head_part, BAR_A_FREE(h), free_ph[h]);
+                epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
                 break;
             }
             if (kStats && threadIdx.x == EPI_WARP0 * 32) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - t_epi));
@@ -711,11 +731,12 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   P.encoding = widths[0] == 65 ? ENC_PE6 : ENC_RAW5;
   P.head_b = B[L - 1][0];
   // fp32 params: biases of hidden layers then head weights
-  std::vector<float> params;
+  std::vector<float> params;   // every vector starts at a multiple of 4 floats (wp[] are multiples of 16)
   std::vector<size_t> bias_off(L);
   for (int l = 0; l < L - 1; ++l) { bias_off[l] = params.size(); params.insert(params.end(), B[l].begin(), B[l].end()); }
   const size_t head_off = params.size();
   params.insert(params.end(), W[L - 1].begin(), W[L - 1].begin() + wp[L - 1]);
+  while (params.size() % 4) params.push_back(0.f);
 
   std::vector<uint16_t> img;
   // forward program: hidden layers 0..L-2, the last one fused with the head
@@ -764,11 +785,17 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   if (cudaMalloc(&out->params, params.size() * 4) != cudaSuccess) { *err = "cudaMalloc (params) failed"; return 4; }
   cudaMemcpy(out->params, params.data(), params.size() * 4, cudaMemcpyHostToDevice);
   const float* pdev = reinterpret_cast<const float*>(out->params);
-  for (int i = 0; i < P.n_fwd; ++i) P.fwd[i].bias = pdev + (size_t)P.fwd[i].bias;
-  for (int i = 0; i < P.n_grad; ++i) P.grad[i].bias = P.grad[i].bias ? pdev + (size_t)P.grad[i].bias : nullptr;
-  // forward step 0's bias offset is 0 -> nullptr check above would drop it for grad step 0; fix explicitly
-  P.grad[0].bias = pdev + bias_off[0];
+  // steps carry the float offset of their bias inside the params block
+  // (staged in shared memory by the kernel)
+  for (int i = 0; i < P.n_grad; ++i) P.grad[i].bias = nullptr;
+  for (int l = 0; l < L - 1; ++l) {
+    P.fwd[l].bias = reinterpret_cast<const float*>(bias_off[l]);
+    P.grad[l].bias = reinterpret_cast<const float*>(bias_off[l]);
+  }
   P.head_w = pdev + head_off;
+  P.params = pdev;
+  P.head_off = (int)head_off;
+  P.params_floats = (int)params.size();
   P.img_fwd = reinterpret_cast<const uint8_t*>(out->img);
   P.img_grad = reinterpret_cast<const uint8_t*>(out->img) + fwd_bytes;
   if (cudaMalloc(&out->dev, sizeof(Prog)) != cudaSuccess) { *err = "cudaMalloc (program) failed"; return 4; }
@@ -788,25 +815,27 @@ constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in per CTA
 template <class Op>
 int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
            uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
-  int kmax = 0, chunk = 0;
+  int kmax = 0, chunk = 0, params_bytes = 0;
   for (int j = 0; j < F.n_obj; ++j) {
     kmax = std::max(kmax, images[j].host.kmax);
     chunk = std::max(chunk, images[j].host.max_chunk_bytes);
+    params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
   }
   const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
-  const int extra = 1024 /*align*/ + 8 * (6 + 2 * 8) + 16 + 2 * ROWS * 4;
+  const int extra = 1024 /*align*/ + 8 * (6 + 2 * 8) + 16 + 2 * ROWS * 4 + params_bytes;
   int n_stages = (SMEM_LIMIT - a_bytes - extra) / chunk;
   n_stages = std::min(n_stages, 8);
   if (n_stages < 2) { *err = "bf16 engine: not enough shared memory for the weight pipeline"; return 1; }
   static const int dbg = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
   if (dbg & 8) n_stages = 8;
+  if (dbg & 256) n_stages = std::min(n_stages, 2);
   const size_t smem = (size_t)a_bytes + (size_t)((dbg & 8) ? 1 : n_stages) * chunk + extra;
   auto kern = mlp_kernel<Op>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
   const int tiles_max = (max_rows + ROWS - 1) / ROWS + (Op::kGrad ? F.n_obj : 0);
   const int grid = std::max(1, std::min(tiles_max, sm_count));
-  kern<<<grid, NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, dbg);
+  kern<<<grid, NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, params_bytes, dbg);
   e = cudaGetLastError();
   if (e != cudaSuccess) { *err = std::string("mlp_kernel launch: ") + cudaGetErrorString(e); return 4; }
   return 0;
