@@ -44,7 +44,8 @@ constexpr int ROWS = 128;
 constexpr bool kStats = DDF_PIPE_STATS != 0;
 __device__ unsigned long long g_dbg[16];
 #define DDF_DBG_T0() long long _t0 = kStats ? clock64() : 0
-#define DDF_DBG_ADD(i) do { if (kStats) atomicAdd(&g_dbg[i], (unsigned long long)(clock64() - _t0)); } while (0)
+#define DDF_DBG_ADD(i) do { if (kStats) dbg_acc[i] += (unsigned long long)(clock64() - _t0); } while (0)
+#define DDF_DBG_FLUSH() do { if (kStats) for (int _i = 0; _i < 16; ++_i) if (dbg_acc[_i]) atomicAdd(&g_dbg[_i], dbg_acc[_i]); } while (0)
 constexpr int NTHREADS = 320;
 constexpr int EPI_WARP0 = 2;
 constexpr int N_EPI_WARPS = 8;
@@ -387,6 +388,9 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
   const uint32_t st_base = smem_u32(S.stages);
   const int tiles = n_tiles(F, op);
   const int sstride = (dbg & 8) ? 0 : stage_bytes;   // dbg 8: all stages alias one buffer (timing only)
+  unsigned long long dbg_acc[16];
+  if (kStats)
+    for (int i = 0; i < 16; ++i) dbg_acc[i] = 0ull;
 
   if (warp == 0) {
     // ================================================= weight producer
@@ -626,7 +630,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                 epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
                 break;
             }
-            if (kStats && threadIdx.x == EPI_WARP0 * 32) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - t_epi));
+            if (kStats && threadIdx.x == EPI_WARP0 * 32) dbg_acc[7] += (unsigned long long)(clock64() - t_epi);
             tc_before_sync();
             if (wa) {
               fence_async_smem();
@@ -651,6 +655,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
       }
     }
   }
+  if (lane == 0 && (warp == 0 || warp == 1 || warp == EPI_WARP0)) DDF_DBG_FLUSH();
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
