@@ -86,6 +86,7 @@ struct Prog {
   int encoding;
   int kmax;            // widest A tile (columns)
   int max_chunk_bytes;
+  int pp;              // 1: two-tile ping-pong program (hidden widths <= 256, one N-half per step)
   float head_b;
   const float* head_w; // fp32, padded last hidden width
   const float* params; // fp32 block: hidden-layer biases then head weights (staged in shared memory)
@@ -660,6 +661,401 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+
+// ================================================================== ping-pong
+// Networks whose hidden layers are at most 256 wide run two 128-row tiles
+// ("slots" X, Y) through the layers in lock-step: the MMA warp issues layer s
+// of X (one full-N chain, N <= 256), then layer s of Y, then s+1 of X...  The
+// epilogue of X's layer s (TMEM -> bias/ReLU -> bf16 A_X) overlaps the MMAs of
+// Y's layer s, so the tensor pipe never waits for an epilogue.  TMEM: X in
+// columns [0, 256), Y in [256, 512).  Each slot has its own A tile, barriers,
+// ReLU-mask scratch and staged params.  The MMAs of a slot's step complete
+// before its epilogue writes the slot's A tile, so no a_free barriers exist.
+
+template <int EPI, int NM>
+__device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
+                                           uint32_t* my_masks, const float* head_w, float& head_part,
+                                           const float* sparams) {
+  const int r7 = r & 7;
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const int c = c_first + i * 64;
+    uint32_t rg[32];
+    DDF_TMEM_LD32(tmem_row + (uint32_t)c, rg);
+    float4 bq[8];
+    uint32_t mq = 0u;
+    if constexpr (EPI != E_BWD_MASK_A) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) bq[k] = *reinterpret_cast<const float4*>(sparams + (size_t)st.bias + c + 4 * k);
+    } else {
+      mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
+    }
+    tmem_wait_ld();
+    const float* bf = reinterpret_cast<const float*>(bq);
+    uint32_t pkd[16];
+    if constexpr (EPI == E_BWD_MASK_A) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pkd[e] = pack_bf16(((mq >> (2 * e)) & 1u) ? __uint_as_float(rg[2 * e]) : 0.f,
+                           ((mq >> (2 * e + 1)) & 1u) ? __uint_as_float(rg[2 * e + 1]) : 0.f);
+    } else if constexpr (EPI == E_RELU_A) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pkd[e] = pack_bf16(fmaxf(__uint_as_float(rg[2 * e]) + bf[2 * e], 0.f),
+                           fmaxf(__uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1], 0.f));
+    } else if constexpr (EPI == E_HEAD) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+      }
+    } else {
+      uint32_t mw = 0u;
+      float v[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float z = __uint_as_float(rg[e]) + bf[e];
+        mw |= (z > 0.f ? 1u : 0u) << e;
+        v[e] = fmaxf(z, 0.f);
+      }
+      if constexpr (EPI == E_RELU_MASK_A) {
+        my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+          v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
+          v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
+          v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
+          v[e + 3] = ((mw >> (e + 3)) & 1u) ? hw.w : 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+    }
+    if constexpr (EPI != E_HEAD) {
+      const uint32_t blk = a_row + (uint32_t)((c >> 6) * (ROWS * 128));
+      const int cc0 = (c & 63) >> 3;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        st_shared_v4(blk + (uint32_t)(((cc0 + e) ^ r7) << 4), pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2],
+                     pkd[4 * e + 3]);
+    }
+  }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_direct_n(int nm, const Step& st, int c_first, int r, uint32_t tmem_row,
+                                             uint32_t a_row, uint32_t* my_masks, const float* head_w,
+                                             float& head_part, const float* sp) {
+  switch (nm) {
+    case 1: epi_direct<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    case 2: epi_direct<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    case 4: epi_direct<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    default: break;
+  }
+}
+
+// Pair p of a CTA -> (objects, row block) of slot `sl`.  Gradient passes pad
+// each object's tile count to even so both slots always run the same network.
+template <class Op>
+__device__ __forceinline__ int pp_pairs(const FieldDev& F, const Op& op) {
+  if constexpr (Op::kGrad) {
+    int t = 0;
+    for (int j = 0; j < F.n_obj; ++j) t += ((op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS + 1) / 2;
+    return t;
+  } else {
+    return ((op.total() + ROWS - 1) / ROWS + 1) / 2;
+  }
+}
+template <class Op>
+__device__ __forceinline__ void pp_rows(const FieldDev& F, const Op& op, int p, int sl, int& j0, int& j1, int& base,
+                                        int& nv) {
+  if constexpr (Op::kGrad) {
+    int j = 0;
+    for (;; ++j) {
+      const int c = ((op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS + 1) / 2;
+      if (p < c || j == F.n_obj - 1) break;
+      p -= c;
+    }
+    base = op.seg_begin(j) + (2 * p + sl) * ROWS;
+    nv = max(0, min(ROWS, op.seg_end(j) - base));
+    j0 = j;
+    j1 = j + 1;
+  } else {
+    base = (2 * p + sl) * ROWS;
+    nv = max(0, min(ROWS, op.total() - base));
+    j0 = 0;
+    j1 = F.n_obj;
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(NTHREADS, 1)
+mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int a_bytes,
+              int stage_bytes, int params_bytes) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* a_tiles = base_ptr;                                   // [2][a_bytes]
+  uint8_t* stages = base_ptr + 2 * (size_t)a_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)n_stages * stage_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * n_stages);
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);           // [2 slots][2 subs][128]
+  float* sparams = red + 4 * ROWS;                                // [2 slots][params_bytes/4]
+  const int pfl = params_bytes >> 2;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar0 = smem_u32(bars);
+  auto BAR_A_READY = [&](int sl) { return bar0 + 8u * sl; };
+  auto BAR_ACC = [&](int sl) { return bar0 + 8u * (2 + sl); };
+  auto BAR_FULL = [&](int s) { return bar0 + 8u * (4 + s); };
+  auto BAR_EMPTY = [&](int s) { return bar0 + 8u * (4 + n_stages + s); };
+
+  if (threadIdx.x == 0) {
+    for (int sl = 0; sl < 2; ++sl) {
+      mbar_init(BAR_A_READY(sl), N_EPI_WARPS);
+      mbar_init(BAR_ACC(sl), 1);
+    }
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(BAR_FULL(s), 1);
+      mbar_init(BAR_EMPTY(s), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t a_base0 = smem_u32(a_tiles);
+  const uint32_t st_base = smem_u32(stages);
+  const int pairs = pp_pairs(F, op);
+
+  if (warp == 0) {
+    // ================================================= weight producer (each step streamed once per slot)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+        int j0, j1, base, nv;
+        pp_rows(F, op, pr, 0, j0, j1, base, nv);
+        for (int j = j0; j < j1; ++j) {
+          const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+          const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
+          for (int s = 0; s < ns; ++s) {
+            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            for (int sl = 0; sl < 2; ++sl) {
+              const uint8_t* src = img + st.img_off;
+              for (int c = 0; c < st.nchunk; ++c) {
+                mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
+                mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
+                bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+                src += st.chunk_bytes;
+                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================= MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t ar[2] = {0u, 0u};
+      for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+        int j0, j1, base, nv;
+        pp_rows(F, op, pr, 0, j0, j1, base, nv);
+        for (int j = j0; j < j1; ++j) {
+          const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+          for (int s = 0; s < ns; ++s) {
+            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            const uint32_t id = idesc(st.rows);
+            for (int sl = 0; sl < 2; ++sl) {
+              // this slot's A tile (and its TMEM columns) are ready
+              mbar_wait(BAR_A_READY(sl), ar[sl] & 1u);
+              ++ar[sl];
+              const uint32_t a_slot = a_base0 + (uint32_t)(sl * a_bytes);
+              for (int kc = 0; kc < st.nchunk; ++kc) {
+                mbar_wait(BAR_FULL(stage), phase);
+                tc_after_sync();
+                const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
+                const uint32_t a_chunk = a_slot + (uint32_t)(kc * ROWS * 128);
+                const uint32_t b_chunk = st_base + (uint32_t)(stage * stage_bytes);
+                for (int ks = 0; ks < nks; ++ks)
+                  mma_bf16(tmem + (uint32_t)(sl * 256), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
+                           (kc | ks) ? 1u : 0u);
+                tc_commit(BAR_EMPTY(stage));
+                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              }
+              tc_commit(BAR_ACC(sl));
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // ================================================= row warps
+    const int q = warp & 3;
+    const int sub = (warp - EPI_WARP0) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    uint32_t acc_ph[2] = {0u, 0u};
+    for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+      int j0 = 0, j1 = 0;
+      int slot_id[2] = {0, 0};
+      bool valid[2] = {false, false};
+      double pos[2][3], az[2], pol[2], best[2] = {0.0, 0.0};
+      int bobj[2] = {0, 0};
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        int base, nv;
+        pp_rows(F, op, pr, sl, j0, j1, base, nv);
+        valid[sl] = r < nv;
+        pos[sl][0] = pos[sl][1] = pos[sl][2] = 0.0;
+        az[sl] = pol[sl] = 0.0;
+        if (valid[sl]) {
+          slot_id[sl] = op.slot(base + r);
+          if constexpr (!Op::kRaw) op.load(slot_id[sl], pos[sl], az[sl], pol[sl]);
+        }
+      }
+      for (int j = j0; j < j1; ++j) {
+        const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+        const NetDev& net = F.net[j];
+        const int head_off = __ldg(&P->head_off);
+        const int k0 = P->k0, halfk = k0 >> 1;
+        double u[2][5];
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          // params of this network for the slot (the slot's previous network is done)
+          {
+            const int nf = __ldg(&P->params_floats);
+            const float4* src = reinterpret_cast<const float4*>(P->params);
+            float4* dst = reinterpret_cast<float4*>(sparams + sl * pfl);
+            named_sync(1, N_EPI_WARPS * 32);
+            for (int i = threadIdx.x - EPI_WARP0 * 32; i < (nf >> 2); i += N_EPI_WARPS * 32) dst[i] = __ldg(src + i);
+            named_sync(1, N_EPI_WARPS * 32);
+          }
+          for (int e = 0; e < 5; ++e) u[sl][e] = 0.0;
+          if constexpr (!Op::kRaw) {
+            if (valid[sl]) row_u(F, j, pos[sl], az[sl], pol[sl], u[sl]);
+          }
+          const uint32_t a_slot = a_base0 + (uint32_t)(sl * a_bytes);
+          for (int c = sub * halfk; c < (sub + 1) * halfk; c += 8) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int k = c + e;
+              float x = 0.f;
+              if (valid[sl]) {
+                if constexpr (Op::kRaw) {
+                  x = (float)op.raw(slot_id[sl], k);
+                } else if (k < 5) {
+                  x = (float)u[sl][k];
+                } else if (net.encoding == ENC_PE6 && k < 5 + 10 * DDF_PE_OCTAVES) {
+                  const int o = (k - 5) / 10, rr = (k - 5) % 10;
+                  float sv, cv;
+                  sincospif(ldexpf((float)u[sl][rr % 5], o), &sv, &cv);
+                  x = rr < 5 ? sv : cv;
+                }
+              }
+              v[e] = x;
+            }
+            st_shared_v4(a_slot + a_off(r, c), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                         pack_bf16(v[6], v[7]));
+          }
+          fence_async_smem();
+          tc_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR_A_READY(sl));
+        }
+
+        const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+        float head_part[2] = {0.f, 0.f};
+        for (int s = 0; s < ns; ++s) {
+          const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+          const int epi = st.epi;
+#pragma unroll
+          for (int sl = 0; sl < 2; ++sl) {
+            mbar_wait(BAR_ACC(sl), acc_ph[sl] & 1u);
+            ++acc_ph[sl];
+            tc_after_sync();
+            const uint32_t tmem_row = tmem + lane_addr + (uint32_t)(sl * 256);
+            uint32_t* my_masks = mask_scratch + ((size_t)blockIdx.x * 2 + sl) * MASK_WORDS_PER_CTA;
+            if (epi == E_BWD_OUT) {
+              if (sub == 0) {
+                float g[128];
+                for (int c = 0; c < st.rows; c += 16) {
+                  uint32_t rg[16];
+                  DDF_TMEM_LD16(tmem_row + (uint32_t)c, rg);
+                  tmem_wait_ld();
+#pragma unroll
+                  for (int e = 0; e < 16; ++e) g[c + e] = __uint_as_float(rg[e]);
+                }
+                if constexpr (Op::kGrad) {
+                  if (valid[sl]) {
+                    if constexpr (Op::kRaw) {
+                      op.store_grad_raw(slot_id[sl], [&](int k) { return (double)g[k]; });
+                    } else {
+                      double g5[5];
+                      pe_chain(net, u[sl], [&](int k) { return (double)g[k]; }, g5);
+                      op.store_grad(slot_id[sl], g5);
+                    }
+                  }
+                }
+              }
+              tc_before_sync();
+              continue;
+            }
+            const uint32_t a_row = a_base0 + (uint32_t)(sl * a_bytes) + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+            const int nm = (st.rows - sub * 32 + 63) >> 6;
+            const float* sp = sparams + sl * pfl;
+            switch (epi) {
+              case E_RELU_A: epi_direct_n<E_RELU_A>(nm, st, sub * 32, r, tmem_row, a_row, my_masks, sp + head_off, head_part[sl], sp); break;
+              case E_RELU_MASK_A: epi_direct_n<E_RELU_MASK_A>(nm, st, sub * 32, r, tmem_row, a_row, my_masks, sp + head_off, head_part[sl], sp); break;
+              case E_MASKG_A: epi_direct_n<E_MASKG_A>(nm, st, sub * 32, r, tmem_row, a_row, my_masks, sp + head_off, head_part[sl], sp); break;
+              case E_BWD_MASK_A: epi_direct_n<E_BWD_MASK_A>(nm, st, sub * 32, r, tmem_row, a_row, my_masks, sp + head_off, head_part[sl], sp); break;
+              default: epi_direct_n<E_HEAD>(nm, st, sub * 32, r, tmem_row, a_row, my_masks, sp + head_off, head_part[sl], sp); break;
+            }
+            tc_before_sync();
+            if (writes_a(epi)) {
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(BAR_A_READY(sl));
+            } else if (epi == E_HEAD) {
+              float* rd = red + sl * 2 * ROWS;
+              rd[sub * ROWS + r] = head_part[sl];
+              named_sync(1, N_EPI_WARPS * 32);
+              if (sub == 0) {
+                double pv = (double)(rd[r] + rd[ROWS + r] + P->head_b);
+                if (F.composite) pv = dmul(net.scale, pv);
+                if (j == j0 || pv < best[sl]) { best[sl] = pv; bobj[sl] = j; }
+              }
+              named_sync(1, N_EPI_WARPS * 32);
+            }
+          }
+        }
+      }
+      if constexpr (!Op::kGrad) {
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl)
+          if (sub == 0 && valid[sl]) op.store_fwd(slot_id[sl], best[sl], bobj[sl]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // ------------------------------------------------------------------ host side
 struct NetImage {
   void* dev = nullptr;       // Prog (device)
@@ -729,8 +1125,12 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
     wo += (size_t)o * in;
     bo += o;
   }
+  int maxh = 0;
+  for (int l = 1; l < L; ++l) maxh = std::max(maxh, wp[l]);
+  const int split = maxh <= 256 ? 1 : 2;   // <= 256: full-N MMAs, two tiles in flight (ping-pong kernel)
   Prog& P = out->host;
   std::memset(&P, 0, sizeof(P));
+  P.pp = split == 1;
   P.k0 = wp[0];
   P.in_width = widths[0];
   P.encoding = widths[0] == 65 ? ENC_PE6 : ENC_RAW5;
@@ -747,7 +1147,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   // forward program: hidden layers 0..L-2, the last one fused with the head
   P.n_fwd = L - 1;
   for (int l = 0; l < L - 1; ++l) {
-    Step s = make_step(wp[l], wp[l + 1], 2, l == L - 2 ? E_HEAD : E_RELU_A);
+    Step s = make_step(wp[l], wp[l + 1], split, l == L - 2 ? E_HEAD : E_RELU_A);
     const std::vector<float>& w = W[l];
     const int K = wp[l];
     append_chunks(img, s, [&](int n, int k) { return w[(size_t)n * K + k]; });
@@ -758,7 +1158,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   std::vector<uint16_t> gimg;
   int gs = 0;
   for (int l = 0; l < L - 1; ++l) {
-    Step s = make_step(wp[l], wp[l + 1], 2, l == L - 2 ? E_MASKG_A : E_RELU_MASK_A);
+    Step s = make_step(wp[l], wp[l + 1], split, l == L - 2 ? E_MASKG_A : E_RELU_MASK_A);
     s.mask_layer = l;
     const std::vector<float>& w = W[l];
     const int K = wp[l];
@@ -769,7 +1169,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   // backward: layer l maps d z_l (width wp[l+1]) to d h_l (width wp[l]) with B[n][k] = W_l[k][n]
   for (int l = L - 2; l >= 0; --l) {
     const bool last = l == 0;
-    Step s = make_step(wp[l + 1], wp[l], last ? 1 : 2, last ? E_BWD_OUT : E_BWD_MASK_A);
+    Step s = make_step(wp[l + 1], wp[l], last ? 1 : split, last ? E_BWD_OUT : E_BWD_MASK_A);
     s.mask_layer = l - 1;
     const std::vector<float>& w = W[l];
     const int Kin = wp[l];
@@ -818,8 +1218,40 @@ inline void free_image(NetImage* im) {
 constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in per CTA
 
 template <class Op>
+int launch_pp(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
+              uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
+  int kmax = 0, chunk = 0, params_bytes = 0;
+  for (int j = 0; j < F.n_obj; ++j) {
+    kmax = std::max(kmax, images[j].host.kmax);
+    chunk = std::max(chunk, images[j].host.max_chunk_bytes);
+    params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
+  }
+  const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
+  const int extra = 1024 + 8 * (4 + 2 * 8) + 16 + 4 * ROWS * 4 + 2 * params_bytes;
+  int n_stages = std::min(8, (SMEM_LIMIT - 2 * a_bytes - extra) / chunk);
+  if (n_stages < 2) { *err = "bf16 ping-pong engine: not enough shared memory"; return 1; }
+  const size_t smem = 2 * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
+  auto kern = mlp_pp_kernel<Op>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
+  const int pairs_max = ((max_rows + ROWS - 1) / ROWS + 1) / 2 + (Op::kGrad ? F.n_obj : 0);
+  const int grid = std::max(1, std::min(pairs_max, sm_count));
+  kern<<<grid, NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, params_bytes);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { *err = std::string("mlp_pp_kernel launch: ") + cudaGetErrorString(e); return 4; }
+  return 0;
+}
+
+template <class Op>
 int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
            uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
+  bool pp = true, any_pp = false;
+  for (int j = 0; j < F.n_obj; ++j) {
+    pp = pp && images[j].host.pp;
+    any_pp = any_pp || images[j].host.pp;
+  }
+  if (any_pp && !pp) { *err = "bf16 engine: networks of one field must all be <= 256 or all > 256 wide"; return 1; }
+  if (pp) return launch_pp<Op>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
   int kmax = 0, chunk = 0, params_bytes = 0;
   for (int j = 0; j < F.n_obj; ++j) {
     kmax = std::max(kmax, images[j].host.kmax);
