@@ -99,7 +99,7 @@ struct ddf_field_s {
   // scratch
   Buf t_acc, t_exit, alive, list, list2, blocks, small, ones;
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
-  Buf pix, rng, umma_masks;
+  Buf pix, rng, umma_masks, st_u34, st_g3;
   int pix_key[6] = {-1, -1, -1, -1, -1, -1};
   int pix_n = 0;
 };
@@ -376,7 +376,7 @@ int ddf_field_destroy(ddf_field_t f) {
   for (auto& im : f->images) umma::free_image(&im);
   Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones,
                  &f->st_o, &f->st_d, &f->st_tacc, &f->st_texit, &f->st_t, &f->st_thr, &f->st_rad,
-                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks};
+                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks, &f->st_u34, &f->st_g3};
   for (Buf* b : bufs) b->release();
   if (f->F_dev) cudaFree(f->F_dev);
   delete f;
@@ -554,6 +554,8 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   CUDA_TRY(f->st_march.ensure(P));
   CUDA_TRY(f->st_alive.ensure(P));
   CUDA_TRY(f->st_obj.ensure(sizeof(int) * P));
+  CUDA_TRY(f->st_u34.ensure(sizeof(double) * 2 * P));
+  CUDA_TRY(f->st_g3.ensure(sizeof(double) * 3 * P));
   CUDA_TRY(f->list.ensure(sizeof(int) * P));
   CUDA_TRY(f->list2.ensure(sizeof(int) * P));
 
@@ -563,9 +565,11 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   S.thr = f->st_thr.as<double>(); S.rad = f->st_rad.as<double>();
   S.hit = f->st_hit.as<uint8_t>(); S.march = f->st_march.as<uint8_t>(); S.alive = f->st_alive.as<uint8_t>();
   S.obj = f->st_obj.as<int>();
+  S.u34 = f->st_u34.as<double>();
+  S.g3 = f->st_g3.as<double>();
   MarchState ms{};
   ms.o = S.o; ms.d = S.d; ms.t_acc = S.t_acc; ms.t_exit = S.t_exit; ms.alive = S.march;
-  ms.t_out = S.t; ms.hit = S.hit; ms.obj = S.obj;
+  ms.t_out = S.t; ms.hit = S.hit; ms.obj = S.obj; ms.u34 = S.u34;
 
   CamDev C{};
   for (int k = 0; k < 3; ++k) {
@@ -606,12 +610,16 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
       int rc = compact_flags(f, S.alive, f->F.n_obj > 1 ? S.obj : nullptr, Pw, f->F.n_obj, f->list.as<int>(),
                              sm.seg, sm.count2, sm.stats + 1, st);
       if (rc) return rc;
-      BounceOp op{};
+      GradOutOp op{};
       op.list = f->list.as<int>(); op.count = sm.count2; op.n = Pw;
       op.seg = f->F.n_obj > 1 ? sm.seg : nullptr;
-      if (f->F.n_obj == 1) op.seg = nullptr;
-      op.F = f->F_dev; op.S = S; op.w = w; op.backoff = f->F.backoff; op.b = b;
+      op.S = S; op.backoff = f->F.backoff;
       if ((rc = run_mlp(f, f->F, op, Pw, true, st))) return rc;
+      {
+        ProfScope ps(f->prof, Prof::OTHER, st);
+        bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->F_dev, w, S, f->list.as<int>(), sm.count2, b);
+        f->prof.launches += 1;
+      }
       if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st))) return rc;
       {
         ProfScope ps(f->prof, Prof::OTHER, st);

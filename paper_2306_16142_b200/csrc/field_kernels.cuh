@@ -44,8 +44,10 @@ __device__ __forceinline__ void pe_chain(const NetDev& net, const double u[5], G
 }
 
 // per-row encoded inputs (before PE) for object j: composite fields see
-// (p - c_j) / s (EXTENSION, config 5); single nets see p (neural.py:35-37)
-__device__ __forceinline__ void row_u(const FieldDev& F, int j, const double* pos, double az, double pol,
+// (p - c_j) / s (EXTENSION, config 5); single nets see p (neural.py:35-37).
+// Row ops hand over the two encoded angle inputs u3 = az/pi - 1,
+// u4 = 2 pol/pi - 1 (neural.py:36-37) already computed.
+__device__ __forceinline__ void row_u(const FieldDev& F, int j, const double* pos, double u3, double u4,
                                       double u[5]) {
   if (F.composite) {
     const NetDev& n = F.net[j];
@@ -53,7 +55,15 @@ __device__ __forceinline__ void row_u(const FieldDev& F, int j, const double* po
   } else {
     for (int c = 0; c < 3; ++c) u[c] = pos[c];
   }
-  encode_angles(az, pol, u[3], u[4]);
+  u[3] = u3;
+  u[4] = u4;
+}
+
+// encoded angle inputs of a unit direction (field.py:77-82 + neural.py:36-37)
+__device__ __forceinline__ void dir_u34(d3 d, double& u3, double& u4) {
+  double az, pol;
+  dir_angles(d, az, pol);
+  encode_angles(az, pol, u3, u4);
 }
 
 __device__ __forceinline__ d3 ld3(const double* a, int64_t i) { return mk3(a[3 * i], a[3 * i + 1], a[3 * i + 2]); }
@@ -100,12 +110,12 @@ struct QueryOp : ListBase {
   double* t; uint8_t* hit; double* pred_out; int* obj_out;
   double delta, thresh;
   __device__ double raw(int, int) const { return 0.0; }
-  __device__ void load(int s, double* p, double& az, double& pol) const {
+  __device__ void load(int s, double* p, double& u3, double& u4) const {
     const d3 q = ld3(pos, s);
     p[0] = q.x; p[1] = q.y; p[2] = q.z;
     double a0, a1;
     dir_angles(ld3(dirs, s), a0, a1);          // field.py:258
-    dir_angles(angles_dir(a0, a1), az, pol);   // field.py:251 re-canonicalise
+    dir_u34(angles_dir(a0, a1), u3, u4);       // field.py:251 re-canonicalise
   }
   __device__ void store_fwd(int s, double pred, int obj) const {
     const double c = fmin(fmax(pred, -delta), delta);   // field.py:253
@@ -121,6 +131,7 @@ struct MarchState {
   const double* o; const double* d;   // (n,3) origins / unit directions
   double* t_acc; const double* t_exit;
   uint8_t* alive; double* t_out; uint8_t* hit; int* obj;
+  const double* u34;                  // (n,2) encoded angles of d, or nullptr (computed per step)
 };
 
 struct TraceStepOp : ListBase {
@@ -128,11 +139,12 @@ struct TraceStepOp : ListBase {
   static constexpr bool kRaw = false;
   MarchState st; double delta, thresh, step;
   __device__ double raw(int, int) const { return 0.0; }
-  __device__ void load(int s, double* p, double& az, double& pol) const {
+  __device__ void load(int s, double* p, double& u3, double& u4) const {
     const d3 o = ld3(st.o, s), d = ld3(st.d, s);
     const double ta = st.t_acc[s];
     p[0] = dadd(o.x, dmul(ta, d.x)); p[1] = dadd(o.y, dmul(ta, d.y)); p[2] = dadd(o.z, dmul(ta, d.z));
-    dir_angles(d, az, pol);
+    if (st.u34) { u3 = st.u34[2 * s]; u4 = st.u34[2 * s + 1]; }
+    else dir_u34(d, u3, u4);
   }
   __device__ void store_fwd(int s, double pred, int obj) const {
     const double c = fmin(fmax(pred, -delta), delta);
@@ -155,7 +167,7 @@ struct NormalOp : ListBase {
   const double* o; const double* d; const double* t_hit;  // t_hit nullable
   double backoff; double* normals; uint8_t* valid;
   __device__ double raw(int, int) const { return 0.0; }
-  __device__ void load(int s, double* p, double& az, double& pol) const {
+  __device__ void load(int s, double* p, double& u3, double& u4) const {
     const d3 oo = ld3(o, s), dd = ld3(d, s);
     if (t_hit) {                                            // field.py:305-307
       const double back = fmax(dsub(t_hit[s], backoff), 0.0);
@@ -163,7 +175,7 @@ struct NormalOp : ListBase {
     } else {
       p[0] = oo.x; p[1] = oo.y; p[2] = oo.z;
     }
-    dir_angles(dd, az, pol);
+    dir_u34(dd, u3, u4);
   }
   __device__ void store_grad(int s, const double* g5) const {
     const d3 g = mk3(g5[0], g5[1], g5[2]);                  // field.py:310-316

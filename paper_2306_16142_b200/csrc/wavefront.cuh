@@ -26,6 +26,8 @@ struct PathState {
   double* thr; double* rad;
   uint8_t* hit; uint8_t* march; uint8_t* alive;
   int* obj;
+  double* u34;                     // (P,2) encoded angles of d (neural.py:36-37), set at ray creation
+  double* g3;                      // (P,3) spatial input gradient from the gradient pass
 };
 
 struct WaveDev {
@@ -49,6 +51,10 @@ __device__ __forceinline__ void slot_sp(const WaveDev& w, int p, int& s, int& i)
 
 // slab test + march initialisation for a new ray (field.py:265-269)
 __device__ __forceinline__ void begin_trace(const FieldDev& F, const PathState& S, int p, d3 o, d3 d) {
+  double u3, u4;
+  dir_u34(d, u3, u4);
+  S.u34[2 * p] = u3;
+  S.u34[2 * p + 1] = u4;
   double te, tx;
   ray_box(o, d, F.lo, F.hi, te, tx);
   const bool in = (te < tx) && (tx > 0.0);
@@ -129,52 +135,63 @@ __device__ __forceinline__ d3 cosine_dir(d3 n, double u0, double u1) {
              dadd(dadd(dmul(l0, t1.z), dmul(l1, t2.z)), dmul(l2, n.z)));
 }
 
-// The fused bounce stage: gradient normal (field.py:295-317) + render.py
-// _hit_normals (127-141) + hit point, throughput, cosine bounce
-// (render.py:226-231) + slab test of the new ray.  Gradient rows only.
-struct BounceOp : ListBase {
+// Gradient pass of a bounce (field.py:295-317 input, render.py:226): the
+// MLP kernel evaluates d pred / d x at o + max(t - delta/2, 0) d with the
+// stored angle inputs and writes the spatial gradient; bounce_kernel below
+// turns it into the normal, hit point and next ray (memory-bound, off the
+// tensor-core critical path).
+struct GradOutOp : ListBase {
   static constexpr bool kGrad = true;
   static constexpr bool kRaw = false;
-  FieldDev const* F;       // device copy (for albedos)
-  PathState S; WaveDev w; double backoff; int b;
+  PathState S; double backoff;
   __device__ double raw(int, int) const { return 0.0; }
-  __device__ void load(int p, double* q, double& az, double& pol) const {
+  __device__ void load(int p, double* q, double& u3, double& u4) const {
     const d3 o = ld3(S.o, p), d = ld3(S.d, p);
     const double back = fmax(dsub(S.t[p], backoff), 0.0);
     q[0] = dadd(o.x, dmul(back, d.x)); q[1] = dadd(o.y, dmul(back, d.y)); q[2] = dadd(o.z, dmul(back, d.z));
-    dir_angles(d, az, pol);
+    u3 = S.u34[2 * p];
+    u4 = S.u34[2 * p + 1];
   }
-  __device__ void store_grad(int p, const double* g5) const {
+  __device__ void store_grad(int p, const double* g5) const { st3(S.g3, p, mk3(g5[0], g5[1], g5[2])); }
+  template <class G>
+  __device__ void store_grad_raw(int, G) const {}
+};
+
+// normal + render.py:_hit_normals (127-141) + hit point, throughput, cosine
+// bounce (render.py:226-231) + slab test of the new ray
+__global__ void bounce_kernel(const FieldDev* F, const WaveDev w, const PathState S, const int* list,
+                              const int* count, int b) {
+  const int n = *count;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int p = list[k];
     const d3 o = ld3(S.o, p), d = ld3(S.d, p);
-    const d3 g = mk3(g5[0], g5[1], g5[2]);
-    const double nr = norm3(g);
-    d3 n;
+    const d3 g = ld3(S.g3, p);
+    const double nr = norm3(g);                              // field.py:311-316
+    d3 nn;
     if (nr >= 1e-12) {
-      n = mk3(ddiv(g.x, nr), ddiv(g.y, nr), ddiv(g.z, nr));
-      if (dot3(n, d) > 0.0) n = mk3(-n.x, -n.y, -n.z);
+      nn = mk3(ddiv(g.x, nr), ddiv(g.y, nr), ddiv(g.z, nr));
+      if (dot3(nn, d) > 0.0) nn = mk3(-nn.x, -nn.y, -nn.z);
     } else {
-      n = mk3(-d.x, -d.y, -d.z);               // render.py:133-136
+      nn = mk3(-d.x, -d.y, -d.z);                            // render.py:133-136
       atomicAdd(w.degenerate, 1ull);
     }
-    if (!(dot3(n, d) < 0.0)) atomicOr(w.err, (int)DEVERR_SIGN_RULE);   // render.py:137-139
+    if (!(dot3(nn, d) < 0.0)) atomicOr(w.err, (int)DEVERR_SIGN_RULE);   // render.py:137-139
     const double t = S.t[p];
-    const d3 hp = mk3(dadd(dadd(o.x, dmul(t, d.x)), dmul(1e-6, n.x)),
-                      dadd(dadd(o.y, dmul(t, d.y)), dmul(1e-6, n.y)),
-                      dadd(dadd(o.z, dmul(t, d.z)), dmul(1e-6, n.z)));
+    const d3 hp = mk3(dadd(dadd(o.x, dmul(t, d.x)), dmul(1e-6, nn.x)),
+                      dadd(dadd(o.y, dmul(t, d.y)), dmul(1e-6, nn.y)),
+                      dadd(dadd(o.z, dmul(t, d.z)), dmul(1e-6, nn.z)));
     const int ob = S.obj[p];
     S.thr[p] = dmul(S.thr[p], F->composite ? F->net[ob].albedo : w.albedo);
     int s, i;
     slot_sp(w, p, s, i);
     double u0, u1;
     pcg_pair(*w.rng, (uint64_t)(s * (w.bounces + 1) + 1 + b) * 2ull * (uint64_t)w.n_pix + 2ull * (uint64_t)i, u0, u1);
-    const d3 nd = cosine_dir(n, u0, u1);
+    const d3 nd = cosine_dir(nn, u0, u1);
     st3(S.o, p, hp);
     st3(S.d, p, nd);
     begin_trace(*F, S, p, hp, nd);
   }
-  template <class G>
-  __device__ void store_grad_raw(int, G) const {}
-};
+}
 
 // render.py:233-242 over the bounce's alive list
 __global__ void after_bounce_kernel(const WaveDev w, const PathState S, const int* list, const int* count) {
