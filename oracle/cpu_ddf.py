@@ -597,3 +597,32 @@ def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None,
 def film_rgb(value, cam: Cam):
     """render.py:244-247 grey -> (H, W, 3)."""
     return np.repeat(value[:, None], 3, axis=1).reshape(cam.height, cam.width, 3)
+
+
+# --------------------------------------------------------------------------
+# single-bounce render modes (render.py:144-184) for the GPU mode parity tests
+# --------------------------------------------------------------------------
+
+def render_mode(fld: Field, cam: Cam, mode: str, background=(0.0, 0.0, 0.0),
+                light_dir=(1.0, 1.0, 1.0), albedo=0.7, env=1.0, ambient=False):
+    """render.py:144-184: "depth" -> (H, W) t (inf on miss); "normal" /
+    "shaded" -> (H, W, 3).  Pixel-centre rays (render.py:62-63)."""
+    n = cam.width * cam.height
+    o, d = camera_rays(cam, np.full((n, 2), 0.5), np.arange(n))
+    t, hit, obj = fld.trace(o, d)
+    if mode == "depth":
+        return np.where(hit, t, np.inf).reshape(cam.height, cam.width)
+    nrm = np.zeros((n, 3))
+    if hit.any():
+        nrm[hit] = hit_normals(fld, o[hit], d[hit], t[hit], obj[hit])
+    rgb = np.empty((n, 3))
+    rgb[:] = np.asarray(background)
+    if mode == "normal":
+        rgb[hit] = 0.5 * (nrm[hit] + 1.0)
+    elif ambient:
+        rgb[hit] = albedo * env
+    else:
+        l = np.asarray(light_dir, dtype=np.float64)
+        l = l / np.linalg.norm(l)
+        rgb[hit] = (albedo * np.maximum(nrm[hit] @ l, 0.0))[:, None]
+    return rgb.reshape(cam.height, cam.width, 3)

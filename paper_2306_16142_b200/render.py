@@ -169,8 +169,129 @@ def render_path(backend, camera, config=None):
     return film_from_accum(accum, camera, config.spp)
 
 
+def pixel_rays(camera, offsets=None):
+    """render.py:54-75 on the host (float64, row-major pixel index)."""
+    w, h = camera.width, camera.height
+    px = np.tile(np.arange(w), h).astype(np.float64)
+    py = np.repeat(np.arange(h), w).astype(np.float64)
+    ox, oy = (0.5, 0.5) if offsets is None else (offsets[:, 0], offsets[:, 1])
+    tan_half = np.tan(camera.vfov / 2.0)
+    sx = (2.0 * (px + ox) / w - 1.0) * tan_half * (w / h)
+    sy = (1.0 - 2.0 * (py + oy) / h) * tan_half
+    d = camera.forward[None, :] + sx[:, None] * camera.right[None, :] + sy[:, None] * camera.up_ortho[None, :]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return np.broadcast_to(camera.position, d.shape).copy(), d
+
+
+def _hit_normals(backend, origins, dirs, t, hit, obj=None):
+    """render.py:127-141: degenerate gradients face the ray; the sign rule
+    n . d < 0 raises NumericError."""
+    from .errors import NumericError
+    normals = np.zeros((len(origins), 3))
+    if hit.any():
+        n, valid = backend.normal_batch(origins[hit], dirs[hit], t_hit=t[hit],
+                                        obj=None if obj is None else obj[hit])
+        bad = ~valid
+        if bad.any():
+            n[bad] = -dirs[hit][bad]
+        if not (np.einsum("ij,ij->i", n, dirs[hit]) < 0.0).all():
+            raise NumericError("normal sign rule violated: n . dir >= 0")
+        normals[hit] = n
+    return normals
+
+
+def _trace_with_obj(backend, o, d):
+    if hasattr(backend, "trace_with_objects"):
+        return backend.trace_with_objects(o, d)
+    t, hit = backend.trace_batch(o, d)
+    return t, hit, None
+
+
+def render_depth(backend, camera, config=None):
+    """render.py:144-150: field values per pixel, non-finite on a miss."""
+    o, d = pixel_rays(camera)
+    t, hit, _ = _trace_with_obj(backend, o, d)
+    return Framebuffer(camera.width, camera.height, np.where(hit, t, np.inf).reshape(camera.height, camera.width))
+
+
+def render_normal(backend, camera, config=None):
+    """render.py:153-164: normals mapped (n + 1)/2, misses get the background."""
+    config = config or RenderConfig(mode="normal")
+    o, d = pixel_rays(camera)
+    t, hit, obj = _trace_with_obj(backend, o, d)
+    nrm = _hit_normals(backend, o, d, t, hit, obj)
+    rgb = np.empty((len(d), 3))
+    rgb[:] = np.asarray(config.background)
+    rgb[hit] = 0.5 * (nrm[hit] + 1.0)
+    return Framebuffer(camera.width, camera.height, rgb.reshape(camera.height, camera.width, 3))
+
+
+def render_shaded(backend, camera, config=None):
+    """render.py:167-184: Lambertian under a directional light (or ambient)."""
+    config = config or RenderConfig(mode="shaded")
+    o, d = pixel_rays(camera)
+    t, hit, obj = _trace_with_obj(backend, o, d)
+    nrm = _hit_normals(backend, o, d, t, hit, obj)
+    rgb = np.empty((len(d), 3))
+    rgb[:] = np.asarray(config.background)
+    if config.ambient:
+        shade = np.full(int(hit.sum()), config.albedo * config.env_radiance)
+    else:
+        l = np.asarray(config.light_dir, dtype=np.float64)
+        shade = config.albedo * np.maximum(nrm[hit] @ (l / np.linalg.norm(l)), 0.0)
+    rgb[hit] = shade[:, None]
+    return Framebuffer(camera.width, camera.height, rgb.reshape(camera.height, camera.width, 3))
+
+
+_MODES = {"depth": render_depth, "normal": render_normal, "shaded": render_shaded, "path": render_path}
+
+
 def render(backend, camera, config):
-    """render.py:258-263 dispatch (path mode is the device wavefront)."""
-    if config.mode == "path":
-        return render_path(backend, camera, config)
-    raise ValueError(f"unknown render mode {config.mode!r}")
+    """render.py:258-263 dispatch."""
+    try:
+        fn = _MODES[config.mode]
+    except KeyError:
+        raise ValueError(f"unknown render mode {config.mode!r}") from None
+    return fn(backend, camera, config)
+
+
+def bench(backends: dict, camera, config, frames: int):
+    """render.py:266-280 (the paper's Fig. 5 timing convention): wall-clock
+    per frame per backend, first frame flagged warm-up.  Rows (backend,
+    frame, ms, warmup)."""
+    import time
+    if frames < 2:
+        raise ValueError("need frames >= 2 to separate warm-up")
+    rows = []
+    for name, backend in backends.items():
+        for i in range(frames):
+            if torch.cuda.is_available():
+                torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            render(backend, camera, config)
+            if torch.cuda.is_available():
+                torch.cuda.synchronize()
+            rows.append((name, i, (time.perf_counter() - t0) * 1e3, 1 if i == 0 else 0))
+    return rows
+
+
+def write_ppm(fb, path, gamma: float = 2.2) -> None:
+    """render.py:283-293 binary P6, 8-bit, gamma-encoded (misses write 0)."""
+    data = fb.data
+    if data.ndim == 2:
+        data = np.repeat(data[:, :, None], 3, axis=2)
+    data = np.where(np.isfinite(data), data, 0.0)
+    u8 = (np.clip(data, 0.0, 1.0) ** (1.0 / gamma) * 255.0 + 0.5).astype(np.uint8)
+    with open(path, "wb") as fh:
+        fh.write(f"P6\n{fb.width} {fb.height}\n255\n".encode("ascii"))
+        fh.write(u8.tobytes())
+
+
+def write_pfm(fb, path) -> None:
+    """render.py:296-303 grayscale little-endian PFM, rows bottom to top."""
+    if fb.data.ndim != 2:
+        raise ValueError("PFM output is for scalar framebuffers")
+    data = np.where(np.isfinite(fb.data), fb.data, 0.0).astype("<f4")
+    with open(path, "wb") as fh:
+        fh.write(f"Pf\n{fb.width} {fb.height}\n-1.0\n".encode("ascii"))
+        fh.write(data[::-1].tobytes())
