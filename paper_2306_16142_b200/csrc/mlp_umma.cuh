@@ -170,6 +170,13 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       : "r"(taddr))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// relu + round-to-nearest bf16 + pack in one instruction (exact: rounding
+// preserves sign, so relu(round(x)) == round(relu(x))); a -> low half
+__device__ __forceinline__ uint32_t pack_bf16_relu(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+  return d;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -207,82 +214,89 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
     for (int e = 0; e < 4; ++e)
       st_shared_v4(blk + (uint32_t)(((cc0 + e) ^ r7) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
   };
-#pragma unroll
-  for (int i = 0; i < NM; ++i) {
-    const int c = c_first + i * 64;
-    uint32_t rg[32];
-    DDF_TMEM_LD32(tmem_row + (uint32_t)c, rg);
-    // this chunk's operands load while the TMEM read is in flight
-    float4 bq[8];
-    uint32_t mq = 0u;
-    if constexpr (BIAS) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        bq[k] = *reinterpret_cast<const float4*>(sparams + (size_t)st.bias + c + 4 * k);   // shared memory
-    } else {
-      mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
-    }
-    tmem_wait_ld();
-    const float* bf = reinterpret_cast<const float*>(bq);
-    uint32_t pkd[16];
-    if constexpr (EPI == E_BWD_MASK_A) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        pkd[e] = pack_bf16(((mq >> (2 * e)) & 1u) ? __uint_as_float(rg[2 * e]) : 0.f,
-                           ((mq >> (2 * e + 1)) & 1u) ? __uint_as_float(rg[2 * e + 1]) : 0.f);
-    } else if constexpr (EPI == E_RELU_A) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        pkd[e] = pack_bf16(fmaxf(__uint_as_float(rg[2 * e]) + bf[2 * e], 0.f),
-                           fmaxf(__uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1], 0.f));
-    } else if constexpr (EPI == E_HEAD) {
-#pragma unroll
-      for (int e = 0; e < 32; e += 4) {
-        const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+  // chunk i's epilogue once its accumulator registers are loaded
+  auto proc = [&](const int i, const int c, const uint32_t (&rg)[32]) {
+      // this chunk's operands load while the TMEM read is in flight
+      float4 bq[8];
+      uint32_t mq = 0u;
+      if constexpr (BIAS) {
+  #pragma unroll
+        for (int k = 0; k < 8; ++k)
+          bq[k] = *reinterpret_cast<const float4*>(sparams + (size_t)st.bias + c + 4 * k);   // shared memory
+      } else {
+        mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
       }
-    } else {
-      // ReLU mask bits of this row's 32 columns (neural.py:241 "h > 0")
-      uint32_t mw = 0u;
-      float v[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const float z = __uint_as_float(rg[e]) + bf[e];
-        mw |= (z > 0.f ? 1u : 0u) << e;
-        v[e] = fmaxf(z, 0.f);
-      }
-      if constexpr (EPI == E_RELU_MASK_A) {
-        my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
-      } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
-#pragma unroll
+      const float* bf = reinterpret_cast<const float*>(bq);
+      uint32_t pkd[16];
+      if constexpr (EPI == E_BWD_MASK_A) {
+  #pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pkd[e] = pack_bf16(((mq >> (2 * e)) & 1u) ? __uint_as_float(rg[2 * e]) : 0.f,
+                             ((mq >> (2 * e + 1)) & 1u) ? __uint_as_float(rg[2 * e + 1]) : 0.f);
+      } else if constexpr (EPI == E_RELU_A) {
+  #pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pkd[e] = pack_bf16_relu(__uint_as_float(rg[2 * e]) + bf[2 * e], __uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1]);
+      } else if constexpr (EPI == E_HEAD) {
+  #pragma unroll
         for (int e = 0; e < 32; e += 4) {
           const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
-          v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
-          v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
-          v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
-          v[e + 3] = ((mw >> (e + 3)) & 1u) ? hw.w : 0.f;
+          head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
+          head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
+          head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
+          head_part = fmaf(fmaxf(__uint_as_float(rg[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+        }
+      } else {
+        // ReLU mask bits of this row's 32 columns (neural.py:241 "h > 0")
+        uint32_t mw = 0u;
+        float v[32];
+  #pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float z = __uint_as_float(rg[e]) + bf[e];
+          mw |= (z > 0.f ? 1u : 0u) << e;
+          v[e] = fmaxf(z, 0.f);
+        }
+        if constexpr (EPI == E_RELU_MASK_A) {
+          my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
+        } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
+  #pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+            v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
+            v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
+            v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
+            v[e + 3] = ((mw >> (e + 3)) & 1u) ? hw.w : 0.f;
+          }
+        }
+  #pragma unroll
+        for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+      }
+      if constexpr (WA) {
+        if (i < HOLD) {
+  #pragma unroll
+          for (int e = 0; e < 16; ++e) hold[i][e] = pkd[e];
+        }
+        if (i == HOLD - 1) {
+          mbar_wait(bar_free, free_ph & 1u);
+          ++free_ph;
+  #pragma unroll
+          for (int q2 = 0; q2 < HOLD; ++q2) store(c_first + q2 * 64, hold[q2]);
+        } else if (i >= HOLD) {
+          store(c, pkd);
         }
       }
+  
+  };
+  // TMEM loads are issued two chunks at a time: tcgen05.wait::ld waits for all
+  // outstanding loads, so pairing halves the exposed TMEM round trips
 #pragma unroll
-      for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
-    }
-    if constexpr (WA) {
-      if (i < HOLD) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) hold[i][e] = pkd[e];
-      }
-      if (i == HOLD - 1) {
-        mbar_wait(bar_free, free_ph & 1u);
-        ++free_ph;
-#pragma unroll
-        for (int q2 = 0; q2 < HOLD; ++q2) store(c_first + q2 * 64, hold[q2]);
-      } else if (i >= HOLD) {
-        store(c, pkd);
-      }
-    }
+  for (int i = 0; i < NM; i += 2) {
+    uint32_t rgA[32], rgB[32];
+    DDF_TMEM_LD32(tmem_row + (uint32_t)(c_first + i * 64), rgA);
+    if (i + 1 < NM) DDF_TMEM_LD32(tmem_row + (uint32_t)(c_first + (i + 1) * 64), rgB);
+    tmem_wait_ld();
+    proc(i, c_first + i * 64, rgA);
+    if (i + 1 < NM) proc(i + 1, c_first + (i + 1) * 64, rgB);
   }
   if constexpr (WA && NM == 0) ++free_ph;   // no columns in this half: keep the phase count in step
 }
@@ -701,8 +715,7 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
     } else if constexpr (EPI == E_RELU_A) {
 #pragma unroll
       for (int e = 0; e < 16; ++e)
-        pkd[e] = pack_bf16(fmaxf(__uint_as_float(rg[2 * e]) + bf[2 * e], 0.f),
-                           fmaxf(__uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1], 0.f));
+        pkd[e] = pack_bf16_relu(__uint_as_float(rg[2 * e]) + bf[2 * e], __uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1]);
     } else if constexpr (EPI == E_HEAD) {
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
