@@ -313,6 +313,67 @@ __device__ __forceinline__ void epi_half(int nmine, const Step& st, int c_first,
   }
 }
 
+// ------------------------------------------------------------------ input encoding
+// bf16 A-tile columns [LO, HI) of one row from its 5 encoded inputs u.  The
+// 6-octave sin/cos encoding (EXTENSION, configs 3-5) takes one sincospif per
+// input and the double-angle recurrence sin 2x = 2 sin x cos x,
+// cos 2x = (cos x - sin x)(cos x + sin x) for the higher octaves: fp32 error
+// ~2^o ulp, far below the bf16 operand rounding.
+__device__ __forceinline__ void pe_tables(const double u[5], float (&sn)[DDF_PE_OCTAVES][5],
+                                          float (&cs)[DDF_PE_OCTAVES][5]) {
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    float sv, cv;
+    sincospif((float)u[j], &sv, &cv);
+    sn[0][j] = sv;
+    cs[0][j] = cv;
+#pragma unroll
+    for (int o = 1; o < DDF_PE_OCTAVES; ++o) {
+      const float s2 = 2.f * sv * cv, c2 = (cv - sv) * (cv + sv);
+      sv = s2;
+      cv = c2;
+      sn[o][j] = sv;
+      cs[o][j] = cv;
+    }
+  }
+}
+template <int LO, int HI>
+__device__ __forceinline__ void store_encoding(bool pe, bool valid, const double u[5], uint32_t a_tile, int r) {
+  float sn[DDF_PE_OCTAVES][5], cs[DDF_PE_OCTAVES][5];
+  if (pe && valid) pe_tables(u, sn, cs);
+#pragma unroll
+  for (int c = LO; c < HI; c += 8) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = c + e;
+      float x = 0.f;
+      if (valid) {
+        if (k < 5) {
+          x = (float)u[k];
+        } else if (pe && k < 5 + 10 * DDF_PE_OCTAVES) {
+          const int o = (k - 5) / 10, rr = (k - 5) % 10;
+          x = rr < 5 ? sn[o][rr] : cs[o][rr - 5];
+        }
+      }
+      v[e] = x;
+    }
+    st_shared_v4(a_tile + a_off(r, c), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                 pack_bf16(v[6], v[7]));
+  }
+}
+// the row's half of the input columns: k0 = 16 (5 raw inputs) or 80 (65 PE inputs)
+__device__ __forceinline__ void encode_row(int k0, int sub, bool pe, bool valid, const double u[5], uint32_t a_tile,
+                                           int r) {
+  if (k0 == 16) {
+    if (sub == 0) store_encoding<0, 8>(false, valid, u, a_tile, r);
+    else store_encoding<8, 16>(false, valid, u, a_tile, r);
+  } else {
+    if (sub == 0) store_encoding<0, 40>(pe, valid, u, a_tile, r);
+    else store_encoding<40, 80>(pe, valid, u, a_tile, r);
+  }
+}
+
 // ------------------------------------------------------------------ tiles
 // Forward: tile t covers list rows [128 t, 128 t + 128) and runs every object.
 // Gradient: tiles enumerate (object, 128-row block) over the object segments.
@@ -552,28 +613,14 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
           if (valid) row_u(F, j, pos, az, pol, u);
         }
         // ---- input encoding -> A columns [sub*k0/2, (sub+1)*k0/2)
-        {
+        if constexpr (!Op::kRaw) {
+          encode_row(P->k0, sub, net.encoding == ENC_PE6, valid, u, a_base, r);
+        } else {
           const int k0 = P->k0, half = k0 >> 1;
           for (int c = sub * half; c < (sub + 1) * half; c += 8) {
             float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int k = c + e;
-              float x = 0.f;
-              if (valid) {
-                if constexpr (Op::kRaw) {
-                  x = (float)op.raw(slot, k);
-                } else if (k < 5) {
-                  x = (float)u[k];
-                } else if (net.encoding == ENC_PE6 && k < 5 + 10 * DDF_PE_OCTAVES) {
-                  const int o = (k - 5) / 10, rr = (k - 5) % 10;
-                  float sv, cv;
-                  sincospif(ldexpf((float)u[rr % 5], o), &sv, &cv);
-                  x = rr < 5 ? sv : cv;
-                }
-              }
-              v[e] = x;
-            }
+            for (int e = 0; e < 8; ++e) v[e] = valid ? (float)op.raw(slot, c + e) : 0.f;
             st_shared_v4(a_base + a_off(r, c), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
                          pack_bf16(v[6], v[7]));
           }
@@ -963,28 +1010,16 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
             if (valid[sl]) row_u(F, j, pos[sl], az[sl], pol[sl], u[sl]);
           }
           const uint32_t a_slot = a_base0 + (uint32_t)(sl * a_bytes);
-          for (int c = sub * halfk; c < (sub + 1) * halfk; c += 8) {
-            float v[8];
+          if constexpr (!Op::kRaw) {
+            encode_row(k0, sub, net.encoding == ENC_PE6, valid[sl], u[sl], a_slot, r);
+          } else {
+            for (int c = sub * halfk; c < (sub + 1) * halfk; c += 8) {
+              float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int k = c + e;
-              float x = 0.f;
-              if (valid[sl]) {
-                if constexpr (Op::kRaw) {
-                  x = (float)op.raw(slot_id[sl], k);
-                } else if (k < 5) {
-                  x = (float)u[sl][k];
-                } else if (net.encoding == ENC_PE6 && k < 5 + 10 * DDF_PE_OCTAVES) {
-                  const int o = (k - 5) / 10, rr = (k - 5) % 10;
-                  float sv, cv;
-                  sincospif(ldexpf((float)u[sl][rr % 5], o), &sv, &cv);
-                  x = rr < 5 ? sv : cv;
-                }
-              }
-              v[e] = x;
+              for (int e = 0; e < 8; ++e) v[e] = valid[sl] ? (float)op.raw(slot_id[sl], c + e) : 0.f;
+              st_shared_v4(a_slot + a_off(r, c), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                           pack_bf16(v[6], v[7]));
             }
-            st_shared_v4(a_slot + a_off(r, c), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                         pack_bf16(v[6], v[7]));
           }
           fence_async_smem();
           tc_before_sync();
