@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the multi-rank logic with several ranks on one GPU")
     return ap.parse_args()
 
 
@@ -169,7 +171,7 @@ def bench_queries(args, rank, world, local):
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     times = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
@@ -303,9 +305,13 @@ def main():
     if name == "c1":
         return bench_queries(args, rank, world, local)
 
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     w = C.WORKLOADS[name]
     prec = args.precision or w["precision"]
     fld = C.build_field(name, precision=prec)
@@ -329,7 +335,7 @@ def main():
 
     per_step = []
     launches = 0
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             flush.zero_()
             if world > 1:

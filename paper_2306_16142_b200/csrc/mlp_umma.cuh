@@ -200,7 +200,8 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 template <int EPI, int NM>
 __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
                                            uint32_t* my_masks, const float* head_w, float& head_part,
-                                           uint32_t bar_free, uint32_t& free_ph, const float* sparams) {
+                                           uint32_t bar_free, uint32_t& free_ph, const float* sparams,
+                                           const uint32_t (&mpre)[4]) {
   constexpr bool WA = EPI == E_RELU_A || EPI == E_RELU_MASK_A || EPI == E_MASKG_A || EPI == E_BWD_MASK_A;
   constexpr bool BIAS = EPI != E_BWD_MASK_A;
   constexpr int HOLD = NM < 2 ? NM : 2;
@@ -224,7 +225,7 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
         for (int k = 0; k < 8; ++k)
           bq[k] = *reinterpret_cast<const float4*>(sparams + (size_t)st.bias + c + 4 * k);   // shared memory
       } else {
-        mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
+        mq = mpre[i];   // prefetched before the accumulator wait
       }
       const float* bf = reinterpret_cast<const float*>(bq);
       uint32_t pkd[16];
@@ -304,12 +305,13 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
 template <int EPI>
 __device__ __forceinline__ void epi_half(int nmine, const Step& st, int c_first, int r, uint32_t tmem_row,
                                          uint32_t a_row, uint32_t* my_masks, const float* head_w, float& head_part,
-                                         uint32_t bar_free, uint32_t& free_ph, const float* sp) {
+                                         uint32_t bar_free, uint32_t& free_ph, const float* sp,
+                                         const uint32_t (&mpre)[4]) {
   switch (nmine) {
-    case 0: epi_chunks<EPI, 0>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
-    case 1: epi_chunks<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
-    case 2: epi_chunks<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
-    default: epi_chunks<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp); break;
+    case 0: epi_chunks<EPI, 0>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    case 1: epi_chunks<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    case 2: epi_chunks<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    default: epi_chunks<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
   }
 }
 
@@ -638,6 +640,14 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
           for (int h = 0; h < st.nh; ++h) {
             const int col0 = h * st.rows;
             const int c_first = col0 + sub * 32;
+            // ReLU mask words of the backward epilogue: load before the wait
+            uint32_t mpre[4] = {0u, 0u, 0u, 0u};
+            if (epi == E_BWD_MASK_A) {
+              const int nm = (st.rows - sub * 32 + 63) >> 6;
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (i < nm) mpre[i] = my_masks[(st.mask_layer * 16 + ((c_first + 64 * i) >> 5)) * ROWS + r];
+            }
             {
               DDF_DBG_T0();
               mbar_wait(BAR_ACC(h), acc_ph[h] & 1u);
@@ -677,19 +687,19 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
             const long long t_epi = kStats ? clock64() : 0;
             switch (epi) {
               case E_RELU_A:
-                epi_half<E_RELU_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
+                epi_half<E_RELU_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_RELU_MASK_A:
-                epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
+                epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_MASKG_A:
-                epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
+                epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_BWD_MASK_A:
-                epi_half<E_BWD_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
+                epi_half<E_BWD_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               default:
-                epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params);
+                epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
             }
             if (kStats && threadIdx.x == EPI_WARP0 * 32) dbg_acc[7] += (unsigned long long)(clock64() - t_epi);
