@@ -162,7 +162,9 @@ int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool 
   ProfScope ps(f->prof, grad ? Prof::GRAD : Prof::FWD, st);
   f->prof.launches += 1;
   (grad ? f->prof.grad_launches : f->prof.fwd_launches) += 1;
-  if (F.precision == PREC_BF16) {
+  bool tensor = F.precision == PREC_BF16;
+  for (int j = 0; j < F.n_obj; ++j) tensor = tensor && F.net[j].wimg_fwd != nullptr;
+  if (tensor) {
     CUDA_TRY(f->umma_masks.ensure(sizeof(uint32_t) * (size_t)umma::MASK_WORDS_PER_CTA * 2 * f->sm_count));
     std::vector<umma::NetImage> imgs;
     if (F.n_obj == 1 && f->F.n_obj > 1) {
@@ -342,9 +344,14 @@ int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths
     N.b[l] = db;
   }
   // bf16 UMMA weight images (built for every net; used when precision == BF16)
-  umma::NetImage img;
-  int rc = umma::build_image(widths, n_widths, weights, biases, &img, &g_err);
-  if (rc) return rc;
+  // A linear model (no hidden layer, a legal reference MlpModel) has no GEMM
+  // for the tensor cores: it runs on the SIMT kernel in both precisions.
+  umma::NetImage img{};
+  img.in_width = widths[0];
+  if (L >= 2) {
+    int rc = umma::build_image(widths, n_widths, weights, biases, &img, &g_err);
+    if (rc) return rc;
+  }
   f->images.push_back(img);
   N.wimg_fwd = img.dev;
   N.wimg_bwd = img.dev;
