@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf"])
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
@@ -152,6 +152,8 @@ def bench_queries(args, rank, world, local):
     from paper_2306_16142_b200 import configs as C
     w = C.WORKLOADS["c1"]
     prec = args.precision or w["precision"]
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     f = C.build_field("c1", precision=prec)
     o, d = C.query_rays(w["n"], 0)
     n = w["n"]
@@ -208,6 +210,108 @@ def bench_queries(args, rank, world, local):
            "gpu_launches": args.steps, "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(out))
+
+
+# ----------------------------------------------------------------- UDF grid
+UDF_RES, UDF_DIRS = 64, 512
+
+
+def cpu_udf(args, reference_line=False):
+    """recon.udf_grid on the CPU (oracle port, float64): a bounded sample of
+    the grid's vertices (every 512th) with the full 512 directions + polish."""
+    from oracle import cpu_ddf as O
+    from paper_2306_16142_b200 import configs as C
+    m = C.models("c1")[0]
+    f = O.Field([O.Net(m.widths, m.v, m.g, m.b)], C.CFG_DELTA, bounds=C.UNIT_BOX)
+    pts = O.grid_points(C.UNIT_BOX, UDF_RES)[::512]
+    O.udf_many(f, pts[:4], UDF_DIRS)
+    reps = max(1, args.steps) if reference_line else 1
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        O.udf_many(f, pts, UDF_DIRS)
+    s = (time.perf_counter() - t0) / reps
+    v = len(pts) / s
+    desc = f"{len(pts)} of the {UDF_RES}^3 grid vertices (every 512th), {UDF_DIRS} dirs + polish, float64 oracle"
+    base = {"value": v, "unit": "udf_points/s", "cores": cpu_cores(), "kind": "port", "sample": desc}
+    if not reference_line:
+        return base
+    return {"impl": "reference", "metric": "udf_points_per_s", "value": v, "unit": "udf_points/s",
+            "n_gpus": args.gpus, "steps": reps, "warmup": 1, "ms_per_step": 1e3 * s, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "udf", "resolution": UDF_RES, "n_dirs": UDF_DIRS, "sample": desc},
+            "cpu_baseline": base, "e2e": {"value": v, "unit": "udf_points/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}
+
+
+def bench_udf(args, rank, world, local):
+    """recon.udf_grid (recon.py:61-81) at 64^3 vertices x 512 directions +
+    golden-section polish on the config-1 network; one step = one grid."""
+    import ctypes
+
+    import torch
+    from paper_2306_16142_b200 import _lib
+    from paper_2306_16142_b200 import configs as C
+    from paper_2306_16142_b200 import udf as U
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    prec = args.precision or "bf16"
+    f = C.build_field("c1", precision=prec)
+    n = UDF_RES ** 3
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    box = (ctypes.c_double * 6)(*np.asarray(C.UNIT_BOX).reshape(-1))
+    L = _lib.lib()
+    st = torch.cuda.current_stream()
+
+    def step():
+        _lib.check(L.ddf_udf_grid(f.handle, box, UDF_RES, UDF_DIRS, 1, ctypes.c_void_p(out.data_ptr()),
+                                  ctypes.c_void_p(st.cuda_stream)))
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    found = int(torch.isfinite(out).sum())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    times = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            step()
+            e1.record(st)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.mean(times))
+    te = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        U.udf_grid(f, resolution=UDF_RES, n_dirs=UDF_DIRS, bounds=C.UNIT_BOX)
+        te.append(time.perf_counter() - t0)
+    queries = n * UDF_DIRS + found * 2 * 2 * 13 * 2        # scan rows + polish probe rows (field.py:456-481)
+    F = C.mlp_flops(C.WORKLOADS["c1"]["widths"])
+    ach = F * queries / (ms / 1e3) / 1e12
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    n_scan = -(-n // ((1 << 25) // UDF_DIRS))
+    # grid points, scan + argmin per chunk, compaction (3) + count, init, 4 x (begin, 13 probes, 12 steps, end), scatter
+    launches = 1 + 2 * n_scan + 3 + 1 + 1 + 4 * 27 + 1
+    res = {"metric": "udf_points_per_s", "value": n / (ms / 1e3), "unit": "udf_points/s", "n_gpus": world,
+           "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+           "config": {"workload": "udf", "resolution": UDF_RES, "n_dirs": UDF_DIRS, "polish": True,
+                      "widths": list(C.WORKLOADS["c1"]["widths"]), "precision": prec,
+                      "l2": "flushed (256 MB write) between timed steps"},
+           "ddf_queries_per_s": queries / (ms / 1e3), "found_points": found,
+           "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                        "traffic": None, "kernel": "fused DDF-MLP (direction scan + polish probes), whole step"},
+           "cpu_baseline": cpu_udf(args) if args.cpu_baseline else None,
+           "e2e": {"value": n / float(np.mean(te)), "unit": "udf_points/s", "h2d_bytes_per_step": 48,
+                   "d2h_bytes_per_step": 8 * n},
+           "gpu_launches": args.steps * launches, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(res))
 
 
 # ----------------------------------------------------------------- clocks
@@ -271,6 +375,10 @@ def main():
             return
         print(json.dumps(cpu_queries(args, reference_line=True)))
         return
+    if args.impl == "reference" and name == "udf":
+        if rank == 0:
+            print(json.dumps(cpu_udf(args, reference_line=True)))
+        return
     if args.impl == "reference":
         if rank != 0:
             return
@@ -304,6 +412,8 @@ def main():
 
     if name == "c1":
         return bench_queries(args, rank, world, local)
+    if name == "udf":
+        return bench_udf(args, rank, world, local)
 
     dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)

@@ -120,6 +120,20 @@ int ddf_normal(ddf_field_t f, const double* origins, const double* dirs, const d
 int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_config_t* cfg, double* accum,
                     ddf_render_stats_t* stats, void* stream);
 
+/* field.udf_many (field.py:418-488) for a neural backend: unsigned distance
+   at n points (device (n,3) f64) = min over the n_dirs Halton sphere
+   directions (field.py:126-141) of query_batch's t (+inf on a miss), then,
+   when polish != 0, two rounds of golden-section search per angle
+   (field.py:450-487).  out (n,) f64 device; +inf where every direction misses.
+   n_dirs >= 1. */
+int ddf_udf(ddf_field_t f, const double* points, int64_t n, int32_t n_dirs, int32_t polish, double* out,
+            void* stream);
+/* recon.udf_grid (recon.py:61-81): ddf_udf at the resolution^3 vertices of
+   the grid over bbox = (lo x, y, z, hi x, y, z) (np.linspace per axis, C
+   order, recon.py:53-58); out (resolution^3,) f64 device.  resolution >= 8. */
+int ddf_udf_grid(ddf_field_t f, const double bbox[6], int32_t resolution, int32_t n_dirs, int32_t polish,
+                 double* out, void* stream);
+
 /* np.random.default_rng(...).random() draw k of a PCG64 stream given its
    (state, inc) (render.py:209,213,222): out[j] = draw idx[j] (device arrays). */
 int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64_t* idx, int64_t n, double* out,

@@ -626,3 +626,109 @@ def render_mode(fld: Field, cam: Cam, mode: str, background=(0.0, 0.0, 0.0),
         l = l / np.linalg.norm(l)
         rgb[hit] = (albedo * np.maximum(nrm[hit] @ l, 0.0))[:, None]
     return rgb.reshape(cam.height, cam.width, 3)
+
+
+# --------------------------------------------------------------------------
+# unsigned distance from the DDF (field.py:115-141, 406-488; recon.py:53-72)
+# --------------------------------------------------------------------------
+
+GOLDEN = (np.sqrt(5.0) - 1.0) / 2.0      # field.py:406  _GOLDEN
+
+
+def van_der_corput(idx, base: int):
+    """field.py:115-123: radical inverse, digits accumulated low to high."""
+    i = np.array(idx, dtype=np.int64)
+    out = np.zeros(len(i))
+    scale = 1.0 / base
+    while (i > 0).any():
+        out += scale * (i % base)
+        i = i // base
+        scale /= base
+    return out
+
+
+def sphere_directions(n: int):
+    """field.py:126-141: Halton(2, 3) -> sphere (z = 1 - 2u, phi = 2 pi v)."""
+    if n < 1:
+        raise ValueError("need at least one direction")
+    k = np.arange(1, n + 1)
+    z = 1.0 - 2.0 * van_der_corput(k, 2)
+    phi = TWO_PI * van_der_corput(k, 3)
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
+
+
+def _query_value(fld: Field, pos, dirs):
+    """field.py:409-413 _eval_angles / 441-442: t on a hit, +inf on a miss."""
+    t, hit = fld.query(pos, dirs)
+    return np.where(hit, t, np.inf)
+
+
+def udf_many(fld: Field, points, n_dirs: int = 512, polish: bool = True):
+    """field.py:418-488 for a neural backend (exact_udf False).
+
+    Stage 1: the minimum over the n_dirs sphere directions; ties resolve to the
+    lowest direction index (the reference's chunked strict-< merge of per-chunk
+    argmins yields exactly the global first argmin).  Stage 2 (polish): two
+    rounds of golden-section search on the polar then azimuth angle, window
+    +-3/sqrt(n_dirs) about the current best, 12 shrink steps, both probes
+    re-evaluated every step, accepted only when strictly better."""
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    dirs = sphere_directions(n_dirs)
+    n = len(pts)
+    vals = _query_value(fld, np.repeat(pts, n_dirs, axis=0), np.tile(dirs, (n, 1))).reshape(n, n_dirs)
+    arg = np.argmin(vals, axis=1)
+    best = vals[np.arange(n), arg]
+    if not polish:
+        return best
+    found = np.isfinite(best)
+    if not found.any():
+        return best
+    p = pts[found]
+    ang = dirs_to_angles(dirs[arg[found]])
+    val = best[found].copy()
+    half = 3.0 / np.sqrt(n_dirs)
+
+    def probe(axis, x):
+        a2 = np.empty_like(ang)
+        a2[:, axis] = x
+        a2[:, 1 - axis] = ang[:, 1 - axis]
+        return _query_value(fld, p, angles_to_dirs(a2))
+
+    for _ in range(2):
+        for axis in (1, 0):
+            lo, hi = ang[:, axis] - half, ang[:, axis] + half
+            if axis == 1:
+                lo, hi = np.clip(lo, 0.0, np.pi), np.clip(hi, 0.0, np.pi)
+            x1, x2 = hi - GOLDEN * (hi - lo), lo + GOLDEN * (hi - lo)
+            f1, f2 = probe(axis, x1), probe(axis, x2)
+            for _ in range(12):
+                right = f1 > f2
+                lo = np.where(right, x1, lo)
+                hi = np.where(right, hi, x2)
+                x1, x2 = hi - GOLDEN * (hi - lo), lo + GOLDEN * (hi - lo)
+                f1, f2 = probe(axis, x1), probe(axis, x2)
+            xs = np.where(f1 < f2, x1, x2)
+            fs = np.minimum(f1, f2)
+            better = fs < val
+            val[better] = fs[better]
+            ang[better, axis] = xs[better]
+    best[found] = val
+    return best
+
+
+def grid_points(bbox, resolution: int):
+    """recon.py:53-58: per-axis linspace of the box corners, ij meshgrid,
+    C order (z fastest)."""
+    bbox = np.asarray(bbox, dtype=np.float64).reshape(2, 3)
+    ax = np.linspace(bbox[0], bbox[1], resolution)
+    x, y, z = np.meshgrid(ax[:, 0], ax[:, 1], ax[:, 2], indexing="ij")
+    return np.stack([x.ravel(), y.ravel(), z.ravel()], axis=1)
+
+
+def udf_grid(fld: Field, resolution: int = 64, n_dirs: int = 512, bounds=None, polish: bool = True):
+    """recon.py:61-81: udf_many at every grid vertex -> (res, res, res)."""
+    if resolution < 8:
+        raise ValueError("resolution must be >= 8")
+    box = np.asarray(bounds if bounds is not None else fld.bounds, dtype=np.float64).reshape(2, 3)
+    return udf_many(fld, grid_points(box, resolution), n_dirs, polish).reshape((resolution,) * 3)

@@ -11,6 +11,7 @@
 #include "ddf_common.cuh"
 #include "field_kernels.cuh"
 #include "mlp_umma.cuh"
+#include "udf.cuh"
 #include "wavefront.cuh"
 
 using namespace ddf;
@@ -100,6 +101,8 @@ struct ddf_field_s {
   Buf t_acc, t_exit, alive, list, list2, blocks, small, ones;
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
   Buf pix, rng, umma_masks, st_u34, st_g3;
+  Buf udf_dirs, udf_vals, udf_pts, udf_best, udf_arg, udf_found, udf_list, udf_seg, udf_state;
+  int udf_ndirs = 0;
   int pix_key[6] = {-1, -1, -1, -1, -1, -1};
   int pix_n = 0;
 };
@@ -244,6 +247,116 @@ void build_stream(const uint64_t st[2], const uint64_t inc[2], PcgStream* out) {
 
 int ensure_small(ddf_field_s* f) {
   CUDA_TRY(f->small.ensure(4096));
+  return DDF_OK;
+}
+
+// ---------------------------------------------------------------- UDF (field.py:418-488)
+__global__ void twice_kernel(const int* c, int* c2) { *c2 = 2 * *c; }
+
+// field.py:115-141 sphere_directions on the host in float64 (setup, not hot)
+std::vector<double> sphere_directions(int n) {
+  auto vdc = [](long long i, int base) {
+    double out = 0.0, scale = 1.0 / base;
+    while (i > 0) {
+      out += scale * (double)(i % base);
+      i /= base;
+      scale /= base;
+    }
+    return out;
+  };
+  const double two_pi = 2.0 * 3.141592653589793;
+  std::vector<double> d(3 * (size_t)n);
+  for (int k = 0; k < n; ++k) {
+    const double z = 1.0 - 2.0 * vdc(k + 1, 2);
+    const double phi = two_pi * vdc(k + 1, 3);
+    const double r = std::sqrt(std::max(0.0, 1.0 - z * z));
+    d[3 * k] = r * std::cos(phi);
+    d[3 * k + 1] = r * std::sin(phi);
+    d[3 * k + 2] = z;
+  }
+  return d;
+}
+
+constexpr int64_t UDF_CHUNK_ROWS = 1ll << 25;   // scan rows per chunk: 256 MB of f64 values
+constexpr int64_t UDF_POLISH_PTS = 1ll << 22;   // points per polish pass: 4M x 76 B of state
+
+int udf_run(ddf_field_s* f, const double* pts, int64_t n, int n_dirs, bool polish, double* out, cudaStream_t st) {
+  if (n_dirs < 1) return fail(DDF_EUSAGE, "need at least one direction");
+  if (n_dirs > (1 << 24)) return fail(DDF_EUSAGE, "n_dirs too large");
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad point count");
+  if (n == 0) return DDF_OK;
+  if (f->udf_ndirs != n_dirs) {
+    const std::vector<double> d = sphere_directions(n_dirs);
+    CUDA_TRY(f->udf_dirs.ensure(sizeof(double) * 5 * n_dirs));     // dirs (n,3) + encoded angles (n,2)
+    CUDA_TRY(cudaMemcpy(f->udf_dirs.p, d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice));
+    udf::dir_u34_kernel<<<(n_dirs + 127) / 128, 128>>>(f->udf_dirs.as<double>(), n_dirs,
+                                                        f->udf_dirs.as<double>() + 3 * n_dirs);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    f->udf_ndirs = n_dirs;
+  }
+  const double* dirs = f->udf_dirs.as<double>();
+  const double* dir_u34 = dirs + 3 * n_dirs;
+  const int64_t pc = std::min<int64_t>(n, UDF_POLISH_PTS);                       // polish pass
+  const int64_t sc = std::max<int64_t>(1, std::min<int64_t>(pc, UDF_CHUNK_ROWS / n_dirs));   // scan chunk
+  CUDA_TRY(f->udf_vals.ensure(sizeof(double) * sc * n_dirs));
+  CUDA_TRY(f->udf_arg.ensure(sizeof(int) * pc));
+  CUDA_TRY(f->udf_found.ensure(pc));
+  CUDA_TRY(f->udf_list.ensure(sizeof(int) * pc));
+  CUDA_TRY(f->udf_seg.ensure(sizeof(int) * 4));
+  if (polish) CUDA_TRY(f->udf_state.ensure(sizeof(double) * 9 * pc));
+  const double golden = (std::sqrt(5.0) - 1.0) / 2.0;        // field.py:406
+  const double half = 3.0 / std::sqrt((double)n_dirs);        // field.py:454
+  for (int64_t q0 = 0; q0 < n; q0 += pc) {
+    const int nq = (int)std::min<int64_t>(pc, n - q0);
+    const double* P = pts + 3 * q0;
+    double* best = out + q0;
+    // stage 1: direction scan + first argmin, chunked by the value buffer
+    for (int64_t p0 = 0; p0 < nq; p0 += sc) {
+      const int np_ = (int)std::min<int64_t>(sc, nq - p0);
+      udf::ScanOp op{};
+      op.list = nullptr; op.count = nullptr; op.n = np_ * n_dirs; op.seg = nullptr;
+      op.pts = P + 3 * p0; op.u34 = dir_u34; op.n_dirs = n_dirs; op.vals = f->udf_vals.as<double>();
+      op.delta = f->F.delta; op.thresh = f->F.thresh;
+      if (int rc = run_mlp(f, f->F, op, op.n, false, st)) return rc;
+      f->prof.launches += 1;
+      udf::reduce_kernel<<<(np_ + 7) / 8, 256, 0, st>>>(op.vals, np_, n_dirs, best + p0,
+                                                         f->udf_arg.as<int>() + p0, f->udf_found.as<uint8_t>() + p0);
+      CUDA_TRY(cudaGetLastError());
+    }
+    if (!polish) continue;
+    // stage 2: golden-section polish of every found point of this pass
+    int* cnt = f->udf_seg.as<int>() + 2;
+    if (int rc = compact_flags(f, f->udf_found.as<uint8_t>(), nullptr, nq, 1, f->udf_list.as<int>(),
+                               f->udf_seg.as<int>(), cnt, nullptr, st))
+      return rc;
+    int* cnt2 = cnt + 1;
+    twice_kernel<<<1, 1, 0, st>>>(cnt, cnt2);
+    double* S = f->udf_state.as<double>();
+    udf::Polish G{f->udf_list.as<int>(), S, S + 2 * pc, S + 3 * pc, S + 4 * pc, S + 5 * pc, S + 6 * pc,
+                  S + 7 * pc, S + 8 * pc};
+    const int nb = (nq + 255) / 256;
+    f->prof.launches += 3;
+    udf::polish_init<<<nb, 256, 0, st>>>(G, f->udf_arg.as<int>(), best, dirs, nq, cnt);
+    udf::ProbeOp pr{};
+    pr.list = nullptr; pr.count = cnt2; pr.n = 2 * nq; pr.seg = nullptr;
+    pr.pts = P; pr.P = G; pr.delta = f->F.delta; pr.thresh = f->F.thresh;
+    for (int round = 0; round < 2; ++round) {
+      for (int axis = 1; axis >= 0; --axis) {                  // field.py:457 (polar, then azimuth)
+        pr.axis = axis;
+        udf::gs_begin<<<nb, 256, 0, st>>>(G, axis, half, golden, nq, cnt);
+        if (int rc = run_mlp(f, f->F, pr, 2 * nq, false, st)) return rc;
+        for (int it = 0; it < 12; ++it) {                       // field.py:476
+          udf::gs_step<<<nb, 256, 0, st>>>(G, golden, nq, cnt);
+          if (int rc = run_mlp(f, f->F, pr, 2 * nq, false, st)) return rc;
+        }
+        udf::gs_end<<<nb, 256, 0, st>>>(G, axis, nq, cnt);
+        f->prof.launches += 14;
+      }
+    }
+    udf::polish_scatter<<<nb, 256, 0, st>>>(G, best, nq, cnt);
+    CUDA_TRY(cudaGetLastError());
+  }
   return DDF_OK;
 }
 
@@ -717,6 +830,29 @@ int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, 
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
   return DDF_OK;
+}
+
+int ddf_udf(ddf_field_t f, const double* points, int64_t n, int32_t n_dirs, int32_t polish, double* out,
+            void* stream) {
+  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  CUDA_TRY(cudaSetDevice(f->device));
+  return udf_run(f, points, n, n_dirs, polish != 0, out, (cudaStream_t)stream);
+}
+
+int ddf_udf_grid(ddf_field_t f, const double bbox[6], int32_t resolution, int32_t n_dirs, int32_t polish,
+                 double* out, void* stream) {
+  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (!bbox) return fail(DDF_EUSAGE, "null bbox");
+  if (resolution < 8) return fail(DDF_EUSAGE, "resolution must be >= 8");   // recon.py:66-67
+  if (resolution > 1024) return fail(DDF_EUSAGE, "resolution too large");
+  CUDA_TRY(cudaSetDevice(f->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = (int64_t)resolution * resolution * resolution;
+  CUDA_TRY(f->udf_pts.ensure(sizeof(double) * 3 * n));
+  udf::grid_points_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      f->udf_pts.as<double>(), resolution, bbox[0], bbox[1], bbox[2], bbox[3], bbox[4], bbox[5]);
+  CUDA_TRY(cudaGetLastError());
+  return udf_run(f, f->udf_pts.as<double>(), n, n_dirs, polish != 0, out, st);
 }
 
 }  // extern "C"

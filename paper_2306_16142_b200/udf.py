@@ -1,0 +1,113 @@
+"""Unsigned distance from the DDF on the GPU (paper Eq. 5).
+
+Mirrors the reference's entry points with the same names, arguments,
+results and errors:
+
+  udf(backend, x, n_dirs, exact, polish)            field.py:388-403
+  udf_many(backend, points, n_dirs, exact, polish)   field.py:418-488
+  udf_grid(backend, resolution, n_dirs, bounds, ...) recon.py:61-81
+  ScalarGrid, grid_points                            recon.py:17-58
+
+The whole computation (direction scan, first argmin, golden-section polish)
+runs on the device through ``ddf_udf`` / ``ddf_udf_grid``; there is no host
+fallback.  Neural backends only: the reference's exact shortcut
+(``backend.exact_distance``) belongs to its mesh backends.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .field import _dev, _ptr, _stream
+
+
+@dataclass
+class ScalarGrid:
+    """recon.py:17-44: UDF values over a box; +inf marks all-miss vertices."""
+    bbox: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.bbox = np.asarray(self.bbox, dtype=np.float64).reshape(2, 3)
+        if self.values.ndim != 3:
+            raise ValueError("grid values must be 3-D")
+        finite = self.values[np.isfinite(self.values)]
+        if finite.size and finite.min() < 0.0:
+            raise ValueError("UDF grid values must be non-negative")
+
+    @property
+    def resolution(self):
+        return self.values.shape
+
+    @property
+    def voxel(self):
+        return (self.bbox[1] - self.bbox[0]) / (np.asarray(self.values.shape) - 1)
+
+    def axes(self):
+        return [np.linspace(self.bbox[0, k], self.bbox[1, k], self.values.shape[k]) for k in range(3)]
+
+
+def grid_points(bbox, resolution: int) -> np.ndarray:
+    """recon.py:47-51 (host copy, for callers; the device builds its own)."""
+    bbox = np.asarray(bbox, dtype=np.float64).reshape(2, 3)
+    ax = np.linspace(bbox[0], bbox[1], resolution)
+    g = np.meshgrid(ax[:, 0], ax[:, 1], ax[:, 2], indexing="ij")
+    return np.stack([c.ravel() for c in g], axis=1)
+
+
+def _check_exact(backend, exact):
+    if exact is None:
+        exact = getattr(backend, "exact_udf", False)
+    if exact:
+        raise ValueError("exact UDF needs a mesh backend (exact_distance); this backend is neural")
+
+
+def udf_many_device(backend, points, n_dirs: int = 512, polish: bool = True, out=None, stream=None):
+    """Device in, device out: points (P, 3) float64 CUDA tensor -> (P,) float64."""
+    if out is None:
+        out = torch.empty(points.shape[0], dtype=torch.float64, device=points.device)
+    s = stream if stream is not None else torch.cuda.current_stream(points.device)
+    _lib.check(_lib.lib().ddf_udf(backend.handle, _ptr(points), points.shape[0], int(n_dirs), int(bool(polish)),
+                                  _ptr(out), ctypes.c_void_p(s.cuda_stream)))
+    return out
+
+
+def udf_many(backend, points, n_dirs: int = 512, exact: bool | None = None, polish: bool = True,
+             chunk: int = 250_000) -> np.ndarray:
+    """field.py:418-488: (P, 3) points -> (P,) distances, +inf = all directions miss.
+    ``chunk`` is accepted for signature parity; the device chunks by itself."""
+    _check_exact(backend, exact)
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    if len(pts) == 0:
+        return np.empty(0)
+    d = _dev(pts, device=backend.torch_device)
+    return udf_many_device(backend, d, n_dirs, polish).cpu().numpy()
+
+
+def udf(backend, x, n_dirs: int = 512, exact: bool | None = None, polish: bool = True):
+    """field.py:388-403: the distance at one point, None when every direction misses."""
+    if n_dirs < 2:
+        raise ValueError("need n_dirs >= 2")
+    v = float(udf_many(backend, np.asarray(x, dtype=np.float64)[None, :], n_dirs=n_dirs, exact=exact,
+                       polish=polish)[0])
+    return None if np.isinf(v) else v
+
+
+def udf_grid(backend, resolution: int = 64, n_dirs: int = 512, bounds=None, exact: bool | None = None,
+             polish: bool = True, chunk_points: int = 32_768) -> ScalarGrid:
+    """recon.py:61-81: the UDF at every vertex of a resolution^3 grid over
+    ``bounds`` (default ``backend.grid_bounds``)."""
+    if resolution < 8:
+        raise ValueError("resolution must be >= 8")
+    _check_exact(backend, exact)
+    box = np.asarray(bounds if bounds is not None else backend.grid_bounds, dtype=np.float64).reshape(2, 3)
+    out = torch.empty(resolution ** 3, dtype=torch.float64, device=backend.torch_device)
+    b6 = (ctypes.c_double * 6)(*box.reshape(-1))
+    _lib.check(_lib.lib().ddf_udf_grid(backend.handle, b6, int(resolution), int(n_dirs), int(bool(polish)),
+                                       _ptr(out), _stream()))
+    return ScalarGrid(box, out.cpu().numpy().reshape(resolution, resolution, resolution))

@@ -130,7 +130,39 @@ def main():
     path = os.path.join(HERE, "reference_golden.npz")
     np.savez_compressed(path, **out)
     print("wrote", path, {k: getattr(v, "shape", None) for k, v in out.items()})
+    main_udf()
+
+
+def main_udf():
+    """field.udf_many (field.py:418-488) and recon.udf_grid (recon.py:61-81).
+    recon imports scikit-image for marching cubes, which is not installed and
+    not on this path: a stub module stands in for that import only."""
+    import types
+    if "skimage" not in sys.modules:
+        sk, skm = types.ModuleType("skimage"), types.ModuleType("skimage.measure")
+        skm.marching_cubes = None
+        sk.measure = skm
+        sys.modules["skimage"], sys.modules["skimage.measure"] = sk, skm
+    from ddfield import recon
+    out = {}
+    mf = field.NeuralField(ref_model(march_net()), 0.1, bounds=UNIT_BOX)
+    pts = np.random.default_rng(4).uniform(-1.0, 1.0, (300, 3))
+    out["u_points"] = pts
+    out["u_dirs64"] = field.sphere_directions(64)
+    out["u_many64_raw"] = field.udf_many(mf, pts, n_dirs=64, polish=False)
+    out["u_many64"] = field.udf_many(mf, pts, n_dirs=64, polish=True)
+    out["u_many16"] = field.udf_many(mf, pts, n_dirs=16, polish=True)
+    out["u_grid8"] = recon.udf_grid(mf, resolution=8, n_dirs=32).values
+    n1 = O.kaiming_uniform_net((5, 128, 128, 128, 128, 1), seed=0)
+    f1 = field.NeuralField(ref_model(n1), DELTA_CFG, bounds=UNIT_BOX)
+    out["u_cfg1_many32"] = field.udf_many(f1, pts[:100], n_dirs=32, polish=True)
+    path = os.path.join(HERE, "reference_golden_udf.npz")
+    np.savez_compressed(path, **out)
+    print("wrote", path, {k: getattr(v, "shape", None) for k, v in out.items()})
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["udf"]:
+        main_udf()
+    else:
+        main()
