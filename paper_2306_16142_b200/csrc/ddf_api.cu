@@ -168,7 +168,7 @@ int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool 
   bool tensor = F.precision == PREC_BF16;
   for (int j = 0; j < F.n_obj; ++j) tensor = tensor && F.net[j].wimg_fwd != nullptr;
   if (tensor) {
-    CUDA_TRY(f->umma_masks.ensure(sizeof(uint32_t) * (size_t)umma::MASK_WORDS_PER_CTA * 2 * f->sm_count));
+    CUDA_TRY(f->umma_masks.ensure(sizeof(uint32_t) * (size_t)umma::MASK_WORDS_PER_CTA * umma::QS * f->sm_count));
     std::vector<umma::NetImage> imgs;
     if (F.n_obj == 1 && f->F.n_obj > 1) {
       // single-network pass (ddf_mlp_*): find which image F.net[0] is

@@ -87,6 +87,7 @@ struct Prog {
   int kmax;            // widest A tile (columns)
   int max_chunk_bytes;
   int pp;              // 1: two-tile ping-pong program (hidden widths <= 256, one N-half per step)
+  int max_hidden;      // widest padded hidden layer (<= 128: four-slot quad kernel)
   float head_b;
   const float* head_w; // fp32, padded last hidden width
   const float* params; // fp32 block: hidden-layer biases then head weights (staged in shared memory)
@@ -743,14 +744,14 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
 // ReLU-mask scratch and staged params.  The MMAs of a slot's step complete
 // before its epilogue writes the slot's A tile, so no a_free barriers exist.
 
-template <int EPI, int NM>
+template <int EPI, int NM, int STRIDE = 64>
 __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
                                            uint32_t* my_masks, const float* head_w, float& head_part,
                                            const float* sparams) {
   const int r7 = r & 7;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    const int c = c_first + i * 64;
+    const int c = c_first + i * STRIDE;
     uint32_t rg[32];
     DDF_TMEM_LD32(tmem_row + (uint32_t)c, rg);
     float4 bq[8];
@@ -829,34 +830,35 @@ __device__ __forceinline__ void epi_direct_n(int nm, const Step& st, int c_first
   }
 }
 
-// Pair p of a CTA -> (objects, row block) of slot `sl`.  Gradient passes pad
-// each object's tile count to even so both slots always run the same network.
-template <class Op>
+// Pack p of a CTA (NS tiles) -> (objects, row block) of slot `sl`.  Gradient
+// passes pad each object's tile count to a multiple of NS so all slots of a
+// pack run the same network.
+template <class Op, int NS = 2>
 __device__ __forceinline__ int pp_pairs(const FieldDev& F, const Op& op) {
   if constexpr (Op::kGrad) {
     int t = 0;
-    for (int j = 0; j < F.n_obj; ++j) t += ((op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS + 1) / 2;
+    for (int j = 0; j < F.n_obj; ++j) t += ((op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS + NS - 1) / NS;
     return t;
   } else {
-    return ((op.total() + ROWS - 1) / ROWS + 1) / 2;
+    return ((op.total() + ROWS - 1) / ROWS + NS - 1) / NS;
   }
 }
-template <class Op>
+template <class Op, int NS = 2>
 __device__ __forceinline__ void pp_rows(const FieldDev& F, const Op& op, int p, int sl, int& j0, int& j1, int& base,
                                         int& nv) {
   if constexpr (Op::kGrad) {
     int j = 0;
     for (;; ++j) {
-      const int c = ((op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS + 1) / 2;
+      const int c = ((op.seg_end(j) - op.seg_begin(j) + ROWS - 1) / ROWS + NS - 1) / NS;
       if (p < c || j == F.n_obj - 1) break;
       p -= c;
     }
-    base = op.seg_begin(j) + (2 * p + sl) * ROWS;
+    base = op.seg_begin(j) + (NS * p + sl) * ROWS;
     nv = max(0, min(ROWS, op.seg_end(j) - base));
     j0 = j;
     j1 = j + 1;
   } else {
-    base = (2 * p + sl) * ROWS;
+    base = (NS * p + sl) * ROWS;
     nv = max(0, min(ROWS, op.total() - base));
     j0 = 0;
     j1 = F.n_obj;
@@ -1115,6 +1117,288 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
 }
 
 // ------------------------------------------------------------------ host side
+// ================================================================== quad
+// Networks whose hidden layers are at most 128 wide (config 1, the UDF scan)
+// run four 128-row tiles ("slots") per CTA, TMEM columns [128 sl, 128 sl + 128).
+// A layer of one slot is only 8 N=128 MMAs (~700 cycles), shorter than one
+// epilogue, so two slots in flight leave the tensor pipe waiting.  Here each
+// group of four row warps owns two slots (group g: slots g and g + 2) and runs
+// whole rows (all columns; the head dot stays in registers, no cross-warp
+// reduction), so the two groups' epilogues overlap each other and the MMAs
+// of the other slots.  Weight chunks are streamed once per layer and shared by
+// the four slots (chunk-major MMA order); params are staged only when the
+// network changes.
+constexpr int QS = 4;
+constexpr int Q_EPI_WARPS = 4 * QS;                      // four row warps per slot
+constexpr int Q_NTHREADS = (EPI_WARP0 + Q_EPI_WARPS) * 32;
+
+template <int EPI>
+__device__ __forceinline__ void epi_rows_n(int nm, const Step& st, int r, uint32_t tmem_row, uint32_t a_row,
+                                           uint32_t* my_masks, const float* head_w, float& head_part,
+                                           const float* sp) {
+  switch (nm) {
+    case 2: epi_direct<EPI, 2, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    case 4: epi_direct<EPI, 4, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ void encode_row_full(int k0, bool pe, bool valid, const double u[5], uint32_t a_tile,
+                                                int r) {
+  if (k0 == 16) store_encoding<0, 16>(false, valid, u, a_tile, r);
+  else store_encoding<0, 80>(pe, valid, u, a_tile, r);
+}
+
+template <class Op>
+__global__ void __launch_bounds__(Q_NTHREADS, 1)
+mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int a_bytes,
+                int stage_bytes, int params_bytes, int dbg) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* a_tiles = base_ptr;                                   // [QS][a_bytes]
+  uint8_t* stages = base_ptr + QS * (size_t)a_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)n_stages * stage_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * QS + 2 * n_stages);
+  float* sparams = reinterpret_cast<float*>(tmem_slot + 4);      // one copy: [params_bytes/4]
+  (void)params_bytes;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar0 = smem_u32(bars);
+  auto BAR_A_READY = [&](int sl) { return bar0 + 8u * sl; };
+  auto BAR_ACC = [&](int sl) { return bar0 + 8u * (QS + sl); };
+  auto BAR_FULL = [&](int s) { return bar0 + 8u * (2 * QS + s); };
+  auto BAR_EMPTY = [&](int s) { return bar0 + 8u * (2 * QS + n_stages + s); };
+
+  if (threadIdx.x == 0) {
+    for (int sl = 0; sl < QS; ++sl) {
+      mbar_init(BAR_A_READY(sl), N_EPI_WARPS / 2);
+      mbar_init(BAR_ACC(sl), 1);
+    }
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(BAR_FULL(s), 1);
+      mbar_init(BAR_EMPTY(s), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t a_base0 = smem_u32(a_tiles);
+  const uint32_t st_base = smem_u32(stages);
+  const int packs = pp_pairs<Op, QS>(F, op);
+  unsigned long long dbg_acc[16];
+  if (kStats)
+    for (int i = 0; i < 16; ++i) dbg_acc[i] = 0ull;
+
+  if (warp == 0) {
+    // ================================================= weight producer: each chunk once per layer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
+        int j0, j1, base, nv;
+        pp_rows<Op, QS>(F, op, pk, 0, j0, j1, base, nv);
+        for (int j = j0; j < j1; ++j) {
+          const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+          const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
+          for (int s = 0; s < ns; ++s) {
+            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            for (int c = 0; c < st.nchunk; ++c) {
+              const uint8_t* src = img + st.img_off + (size_t)c * st.chunk_bytes;
+              DDF_DBG_T0();
+              mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
+              DDF_DBG_ADD(6);
+              mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
+              bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+              if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================= MMA issuer: chunk-major over the four slots
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t ar[QS] = {0u, 0u, 0u, 0u};
+      const long long t_all = kStats ? clock64() : 0;
+      for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
+        int j0, j1, base, nv;
+        pp_rows<Op, QS>(F, op, pk, 0, j0, j1, base, nv);
+        for (int j = j0; j < j1; ++j) {
+          const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+          for (int s = 0; s < ns; ++s) {
+            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            const uint32_t id = idesc(st.rows);
+            for (int kc = 0; kc < st.nchunk; ++kc) {
+              {
+                DDF_DBG_T0();
+                mbar_wait(BAR_FULL(stage), phase);
+                DDF_DBG_ADD(1);
+              }
+              tc_after_sync();
+              const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
+              const uint32_t b_chunk = st_base + (uint32_t)(stage * stage_bytes);
+#pragma unroll 1
+              for (int sl = 0; sl < QS; ++sl) {
+                if (kc == 0) {
+                  // this slot's A tile is written and its TMEM columns are read out
+                  DDF_DBG_T0();
+                  mbar_wait(BAR_A_READY(sl), ar[sl] & 1u);
+                  DDF_DBG_ADD(0);
+                  ++ar[sl];
+                  tc_after_sync();
+                }
+                const uint32_t a_chunk = a_base0 + (uint32_t)(sl * a_bytes) + (uint32_t)(kc * ROWS * 128);
+                for (int ks = 0; ks < nks; ++ks)
+                  mma_bf16(tmem + (uint32_t)(sl * 128), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
+                           (kc | ks) ? 1u : 0u);
+                if (kc == st.nchunk - 1) tc_commit(BAR_ACC(sl));
+              }
+              tc_commit(BAR_EMPTY(stage));
+              if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+            }
+          }
+        }
+      }
+      if (kStats) dbg_acc[4] += (unsigned long long)(clock64() - t_all);
+    }
+  } else {
+    // ================================================= row warps: group g (four warps, one per TMEM
+    // lane quarter) owns slot g, so the four slots' epilogues run concurrently
+    const int q = warp & 3;
+    const int sl = (warp - EPI_WARP0) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t tmem_row = tmem + lane_addr + (uint32_t)(sl * 128);
+    const uint32_t a_slot = a_base0 + (uint32_t)(sl * a_bytes);
+    const uint32_t a_row = a_slot + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+    uint32_t* my_masks = mask_scratch + ((size_t)blockIdx.x * QS + sl) * MASK_WORDS_PER_CTA;
+    uint32_t acc_ph = 0u;
+    int staged = -1;
+    const bool w0 = kStats && threadIdx.x == EPI_WARP0 * 32;
+    const long long t_rows = kStats ? clock64() : 0;
+    for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
+      long long t_ph = kStats ? clock64() : 0;
+      int j0, j1, base, nv;
+      pp_rows<Op, QS>(F, op, pk, sl, j0, j1, base, nv);
+      const bool valid = r < nv;
+      int slot_id = 0;
+      double pos[3] = {0.0, 0.0, 0.0}, az = 0.0, pol = 0.0, best = 0.0;
+      int bobj = 0;
+      if (valid) {
+        slot_id = op.slot(base + r);
+        if constexpr (!Op::kRaw) op.load(slot_id, pos, az, pol);
+      }
+      if (w0) { dbg_acc[3] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
+      for (int j = j0; j < j1; ++j) {
+        const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
+        const NetDev& net = F.net[j];
+        const int head_off = __ldg(&P->head_off);
+        const int k0 = P->k0;
+        if (j != staged) {
+          // every row warp is past its last read of the previous network's params
+          const int nf = __ldg(&P->params_floats);
+          const float4* src = reinterpret_cast<const float4*>(P->params);
+          float4* dst = reinterpret_cast<float4*>(sparams);
+          named_sync(1, Q_EPI_WARPS * 32);
+          for (int i = threadIdx.x - EPI_WARP0 * 32; i < (nf >> 2); i += Q_EPI_WARPS * 32) dst[i] = __ldg(src + i);
+          named_sync(1, Q_EPI_WARPS * 32);
+          staged = j;
+          if (w0) { dbg_acc[8] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
+        }
+        double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        if constexpr (!Op::kRaw) {
+          if (valid) row_u(F, j, pos, az, pol, u);
+          encode_row_full(k0, net.encoding == ENC_PE6, valid, u, a_slot, r);
+        } else {
+          for (int c = 0; c < k0; c += 8) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = valid ? (float)op.raw(slot_id, c + e) : 0.f;
+            st_shared_v4(a_slot + a_off(r, c), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                         pack_bf16(v[6], v[7]));
+          }
+        }
+        fence_async_smem();
+        tc_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR_A_READY(sl));
+        if (w0) { dbg_acc[5] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
+
+        const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+        float head_part = 0.f;
+        for (int s = 0; s < ns; ++s) {
+          const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+          const int epi = st.epi;
+          mbar_wait(BAR_ACC(sl), acc_ph & 1u);
+          if (w0) { dbg_acc[2] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
+          ++acc_ph;
+          tc_after_sync();
+          if (epi == E_BWD_OUT) {
+            float gr[128];
+            for (int c = 0; c < st.rows; c += 16) {
+              uint32_t rg[16];
+              DDF_TMEM_LD16(tmem_row + (uint32_t)c, rg);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 16; ++e) gr[c + e] = __uint_as_float(rg[e]);
+            }
+            if constexpr (Op::kGrad) {
+              if (valid) {
+                if constexpr (Op::kRaw) {
+                  op.store_grad_raw(slot_id, [&](int kk) { return (double)gr[kk]; });
+                } else {
+                  double g5[5];
+                  pe_chain(net, u, [&](int kk) { return (double)gr[kk]; }, g5);
+                  op.store_grad(slot_id, g5);
+                }
+              }
+            }
+            tc_before_sync();
+            continue;
+          }
+          const int nm = (dbg & 1024) ? 0 : st.rows >> 5;   // dbg 1024: timing only, no epilogue arithmetic
+          switch (epi) {
+            case E_RELU_A: epi_rows_n<E_RELU_A>(nm, st, r, tmem_row, a_row, my_masks, sparams + head_off, head_part, sparams); break;
+            case E_RELU_MASK_A: epi_rows_n<E_RELU_MASK_A>(nm, st, r, tmem_row, a_row, my_masks, sparams + head_off, head_part, sparams); break;
+            case E_MASKG_A: epi_rows_n<E_MASKG_A>(nm, st, r, tmem_row, a_row, my_masks, sparams + head_off, head_part, sparams); break;
+            case E_BWD_MASK_A: epi_rows_n<E_BWD_MASK_A>(nm, st, r, tmem_row, a_row, my_masks, sparams + head_off, head_part, sparams); break;
+            default: epi_rows_n<E_HEAD>(nm, st, r, tmem_row, a_row, my_masks, sparams + head_off, head_part, sparams); break;
+          }
+          tc_before_sync();
+          if (writes_a(epi)) {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR_A_READY(sl));
+          } else if (epi == E_HEAD) {
+            double pv = (double)(head_part + P->head_b);
+            if (F.composite) pv = dmul(net.scale, pv);
+            if (j == j0 || pv < best) { best = pv; bobj = j; }
+          }
+          if (w0) { dbg_acc[7] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
+        }
+      }
+      if constexpr (!Op::kGrad) {
+        if (valid) op.store_fwd(slot_id, best, bobj);
+      }
+      if (w0) dbg_acc[10] += (unsigned long long)(clock64() - t_ph);
+    }
+    if (w0) dbg_acc[9] += (unsigned long long)(clock64() - t_rows);
+  }
+  if (kStats && lane == 0 && (warp == 0 || warp == 1 || warp == EPI_WARP0)) DDF_DBG_FLUSH();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 struct NetImage {
   void* dev = nullptr;       // Prog (device)
   void* img = nullptr;       // fwd + grad images
@@ -1189,6 +1473,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   Prog& P = out->host;
   std::memset(&P, 0, sizeof(P));
   P.pp = split == 1;
+  P.max_hidden = maxh;
   P.k0 = wp[0];
   P.in_width = widths[0];
   P.encoding = widths[0] == 65 ? ENC_PE6 : ENC_RAW5;
@@ -1301,8 +1586,38 @@ int launch_pp(const FieldDev& F, const std::vector<NetImage>& images, const Op& 
 }
 
 template <class Op>
+int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
+                uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
+  int kmax = 0, chunk = 0, params_bytes = 0;
+  for (int j = 0; j < F.n_obj; ++j) {
+    kmax = std::max(kmax, images[j].host.kmax);
+    chunk = std::max(chunk, images[j].host.max_chunk_bytes);
+    params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
+  }
+  const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
+  const int extra = 1024 + 8 * (2 * QS + 2 * 8) + 16 + params_bytes;
+  int n_stages = std::min(8, (SMEM_LIMIT - QS * a_bytes - extra) / chunk);
+  if (n_stages < 2) { *err = "bf16 quad engine: not enough shared memory"; return 1; }
+  const size_t smem = QS * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
+  auto kern = mlp_quad_kernel<Op>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
+  const int packs_max = ((max_rows + ROWS - 1) / ROWS + QS - 1) / QS + (Op::kGrad ? F.n_obj : 0);
+  const int grid = std::max(1, std::min(packs_max, sm_count));
+  static const int dbg = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
+  kern<<<grid, Q_NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, params_bytes, dbg);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { *err = std::string("mlp_quad_kernel launch: ") + cudaGetErrorString(e); return 4; }
+  return 0;
+}
+
+template <class Op>
 int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
            uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
+  static const int dbgq = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
+  bool quad = !(dbgq & 512);
+  for (int j = 0; j < F.n_obj; ++j) quad = quad && images[j].host.pp && images[j].host.max_hidden <= 128;
+  if (quad) return launch_quad<Op>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
   bool pp = true, any_pp = false;
   for (int j = 0; j < F.n_obj; ++j) {
     pp = pp && images[j].host.pp;

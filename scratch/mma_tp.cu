@@ -17,11 +17,18 @@ __global__ void k(int nmma, int n, int mode, unsigned long long* out) {
   asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads(); asm volatile("tcgen05.fence::after_thread_sync;");
   uint32_t tmem = tslot;
   uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  uint32_t a = smem_u32(base), b = smem_u32(base + 65536);
+  uint32_t a = smem_u32(base), b = smem_u32(base + 131072);
+  if ((mode & 16) && threadIdx.x >= 64) {   // 8 warps storing 16-byte vectors into a separate region
+    const uint32_t w = smem_u32(base + 163840) + (threadIdx.x - 64) * 16;
+    for (int it = 0; it < nmma * 2; ++it)
+      asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" :: "r"(w + (uint32_t)((it & 7) * 4096)), "r"(it) : "memory");
+  }
   long long t0 = clock64();
   if (threadIdx.x == 0) {
     for (int i = 0; i < nmma; ++i) {
-      uint64_t ad = sdesc(a + (i & 3) * 32), bd = sdesc(b + (i & 3) * 32);
+      const uint32_t kc = (mode & 8) ? (uint32_t)((i >> 2) & 1) * 16384u : 0u;
+      const uint32_t sl = (mode & 8) ? (uint32_t)((i >> 3) & 3) * 32768u : 0u;
+      uint64_t ad = sdesc(a + sl + kc + (i & 3) * 32), bd = sdesc(b + kc + (i & 3) * 32);
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
                    :: "r"(tmem + (uint32_t)((mode & 2) ? ((i >> 2) & 1) * n : 0)), "l"(ad), "l"(bd), "r"(idesc), "r"((uint32_t)(i & 3)));
       if ((i & 3) == 3 && (mode & 4)) {   // a pre-completed barrier wait per chunk
@@ -43,14 +50,14 @@ __global__ void k(int nmma, int n, int mode, unsigned long long* out) {
 }
 int main() {
   unsigned long long* d; cudaMalloc(&d, 8);
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   int ns[] = {64, 128, 256};
-  for (int mode : {1, 5}) for (int n : ns) {
+  for (int mode : {1, 9, 17, 25}) for (int n : ns) {
     int nmma = 4096;
     cudaMemset(d, 0, 8);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k<<<148, 128, 200 * 1024>>>(nmma, n, mode, d);
+    k<<<148, 320, 220 * 1024>>>(nmma, n, mode, d);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long cyc; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
