@@ -120,6 +120,22 @@ int ddf_normal(ddf_field_t f, const double* origins, const double* dirs, const d
 int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_config_t* cfg, double* accum,
                     ddf_render_stats_t* stats, void* stream);
 
+/* Exact triangle-mesh field: the reference's OracleField (field.py:191-200)
+   over a TriangleMesh (mesh.py:19-67) with its BVH (mesh.py:94-166), built
+   once from HOST arrays vertices (nv,3) f64 and faces (nf,3) int32.
+   DDF_EDATA for an empty mesh or an out-of-range face index.  The handle
+   works with ddf_query / ddf_trace (t, hit; obj receives the hit face id),
+   ddf_normal (re-intersect, face normal, n . d < 0; t_hit and obj unused)
+   and ddf_render_path (the BVH side of the paper's DDF-vs-BVH timing). */
+int ddf_mesh_create(const double* vertices, int64_t n_vertices, const int32_t* faces, int64_t n_faces,
+                    int32_t device, ddf_field_t* out);
+/* mesh.intersect_rays (mesh.py:264-279) == _kernels.bvh_intersect_batch
+   (_kernels.py:207-219): nearest hit with t in [t_min, t_max]; face -1 on a
+   miss (t = inf, u = v = 0); ties on t go to the lower face index.  Device
+   arrays; face/t/u/v nullable. */
+int ddf_mesh_intersect(ddf_field_t f, const double* origins, const double* dirs, int64_t n, double t_min,
+                       double t_max, int64_t* face, double* t, double* u, double* v, void* stream);
+
 /* field.udf_many (field.py:418-488) for a neural backend: unsigned distance
    at n points (device (n,3) f64) = min over the n_dirs Halton sphere
    directions (field.py:126-141) of query_batch's t (+inf on a miss), then,

@@ -732,3 +732,103 @@ def udf_grid(fld: Field, resolution: int = 64, n_dirs: int = 512, bounds=None, p
         raise ValueError("resolution must be >= 8")
     box = np.asarray(bounds if bounds is not None else fld.bounds, dtype=np.float64).reshape(2, 3)
     return udf_many(fld, grid_points(box, resolution), n_dirs, polish).reshape((resolution,) * 3)
+
+
+# --------------------------------------------------------------------------
+# exact triangle-mesh field (field.py:144-200, mesh.py:264-279, _kernels.py:43-147)
+# --------------------------------------------------------------------------
+
+DET_EPS = 1e-9               # _kernels.py:16
+
+
+def ray_tri(o, d, a, b, c):
+    """_kernels.py:43-77 Moller-Trumbore, elementwise over broadcast arrays in
+    the reference's operation order.  Returns (t, u, v); t = inf on a miss."""
+    e1 = [b[..., k] - a[..., k] for k in range(3)]
+    e2 = [c[..., k] - a[..., k] for k in range(3)]
+    dx, dy, dz = d[..., 0], d[..., 1], d[..., 2]
+    hx = dy * e2[2] - dz * e2[1]
+    hy = dz * e2[0] - dx * e2[2]
+    hz = dx * e2[1] - dy * e2[0]
+    det = e1[0] * hx + e1[1] * hy + e1[2] * hz
+    ok = ~((-DET_EPS < det) & (det < DET_EPS))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        f = 1.0 / det
+        sx, sy, sz = o[..., 0] - a[..., 0], o[..., 1] - a[..., 1], o[..., 2] - a[..., 2]
+        u = f * (sx * hx + sy * hy + sz * hz)
+        ok &= ~((u < 0.0) | (u > 1.0))
+        qx = sy * e1[2] - sz * e1[1]
+        qy = sz * e1[0] - sx * e1[2]
+        qz = sx * e1[1] - sy * e1[0]
+        v = f * (dx * qx + dy * qy + dz * qz)
+        ok &= ~((v < 0.0) | (u + v > 1.0))
+        t = f * (e2[0] * qx + e2[1] * qy + e2[2] * qz)
+    return np.where(ok, t, np.inf), np.where(ok, u, 0.0), np.where(ok, v, 0.0)
+
+
+class MeshField:
+    """The reference's exact mesh backend (BruteForceField semantics, equal to
+    OracleField): every query scans all faces; nearest t in [t_min, t_max],
+    ties to the lower face index (_kernels.py:130-147)."""
+
+    composite = False
+    albedos = None
+
+    def __init__(self, vertices, faces, chunk: int = 1 << 22):
+        self.vertices = np.asarray(vertices, dtype=np.float64)
+        self.faces = np.asarray(faces, dtype=np.int32)
+        lo, hi = self.vertices.min(axis=0), self.vertices.max(axis=0)
+        diag = float(np.linalg.norm(hi - lo))
+        self.bounds = np.stack([lo - diag, hi + diag])                  # field.py:154-157
+        self.grid_bounds = np.stack([lo - 0.05 * diag, hi + 0.05 * diag])
+        tri = self.vertices[self.faces]
+        self._a, self._b, self._c = tri[:, 0], tri[:, 1], tri[:, 2]
+        self._chunk = chunk
+
+    def intersect(self, o, d, t_min=0.0, t_max=np.inf):
+        """mesh.intersect_rays (mesh.py:264-279) -> (face, t, u, v)."""
+        o = np.atleast_2d(np.asarray(o, dtype=np.float64))
+        d = np.atleast_2d(np.asarray(d, dtype=np.float64))
+        n, m = len(o), len(self.faces)
+        face = np.full(n, -1, np.int64)
+        t_out, u_out, v_out = np.full(n, np.inf), np.zeros(n), np.zeros(n)
+        step = max(1, self._chunk // max(m, 1))
+        for s in range(0, n, step):
+            oo, dd = o[s:s + step, None, :], d[s:s + step, None, :]
+            t, u, v = ray_tri(oo, dd, self._a[None], self._b[None], self._c[None])
+            t = np.where((t_min <= t) & (t <= t_max), t, np.inf)
+            k = np.argmin(t, axis=1)                 # first minimum = lowest face index
+            r = np.arange(len(k))
+            tk = t[r, k]
+            hit = np.isfinite(tk)
+            face[s:s + step] = np.where(hit, k, -1)
+            t_out[s:s + step] = tk
+            u_out[s:s + step] = np.where(hit, u[r, k], 0.0)
+            v_out[s:s + step] = np.where(hit, v[r, k], 0.0)
+        return face, t_out, u_out, v_out
+
+    def query(self, pos, dirs):
+        """field.py:161-165."""
+        face, t, _, _ = self.intersect(pos, dirs)
+        return t, face >= 0
+
+    def trace(self, o, d, log=None):
+        """field.py:168 (trace_batch = query_batch); obj = the hit face."""
+        face, t, _, _ = self.intersect(o, d)
+        return t, face >= 0, face.astype(np.int32)
+
+    def normal(self, o, d, t_hit=None, obj=None):
+        """field.py:172-189: re-intersect, face normal, flipped so n . d <= 0."""
+        d = np.atleast_2d(d)
+        face, _, _, _ = self.intersect(o, d)
+        valid = face >= 0
+        n = np.zeros((len(d), 3))
+        if valid.any():
+            fv = self.faces[face[valid]]
+            v = self.vertices
+            nn = np.cross(v[fv[:, 1]] - v[fv[:, 0]], v[fv[:, 2]] - v[fv[:, 0]])
+            nn /= np.linalg.norm(nn, axis=1, keepdims=True)
+            dots = np.einsum("ij,ij->i", nn, d[valid])
+            nn[dots > 0.0] *= -1.0
+            n[valid] = nn
+        return n, valid

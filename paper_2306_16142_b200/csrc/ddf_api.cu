@@ -12,6 +12,7 @@
 #include "field_kernels.cuh"
 #include "mlp_umma.cuh"
 #include "udf.cuh"
+#include "mesh.cuh"
 #include "wavefront.cuh"
 
 using namespace ddf;
@@ -102,6 +103,9 @@ struct ddf_field_s {
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
   Buf pix, rng, umma_masks, st_u34, st_g3;
   Buf udf_dirs, udf_vals, udf_pts, udf_best, udf_arg, udf_found, udf_list, udf_seg, udf_state;
+  // exact mesh field (ddf_mesh_create)
+  mesh::MeshDev M{};
+  Buf mesh_nodes, mesh_tris, mesh_tof;
   int udf_ndirs = 0;
   int pix_key[6] = {-1, -1, -1, -1, -1, -1};
   int pix_n = 0;
@@ -247,6 +251,95 @@ void build_stream(const uint64_t st[2], const uint64_t inc[2], PcgStream* out) {
 
 int ensure_small(ddf_field_s* f) {
   CUDA_TRY(f->small.ensure(4096));
+  return DDF_OK;
+}
+
+bool has_geometry(const ddf_field_s* f) { return f && (f->F.n_obj > 0 || f->F.is_mesh); }
+
+// ---------------------------------------------------------------- mesh BVH (mesh.py:94-166)
+// Median split on the longest box axis, <= 4 triangles per leaf, built once
+// on the host.  The partition (std::nth_element) may order equal centroids
+// differently from numpy's argpartition; hits do not depend on the tree.
+int build_mesh(ddf_field_s* f, const double* V, int64_t nv, const int32_t* Fc, int64_t nf) {
+  using mesh::Node;
+  using mesh::Tri;
+  const int LEAF = 4;
+  std::vector<double> tmin(3 * nf), tmax(3 * nf), cent(3 * nf);
+  for (int64_t i = 0; i < nf; ++i) {
+    for (int k = 0; k < 3; ++k) {
+      const double a = V[3 * Fc[3 * i] + k], b = V[3 * Fc[3 * i + 1] + k], c = V[3 * Fc[3 * i + 2] + k];
+      tmin[3 * i + k] = std::min(std::min(a, b), c);
+      tmax[3 * i + k] = std::max(std::max(a, b), c);
+      cent[3 * i + k] = ((a + b) + c) / 3.0;
+    }
+  }
+  std::vector<int> prim(nf);
+  for (int64_t i = 0; i < nf; ++i) prim[i] = (int)i;
+  std::vector<Node> nodes;
+  nodes.reserve(2 * (size_t)(nf / LEAF + 1));
+  struct Job { int node, lo, hi; };
+  std::vector<Job> stack;
+  nodes.push_back(Node{});
+  stack.push_back({0, 0, (int)nf});
+  while (!stack.empty()) {
+    const Job j = stack.back();
+    stack.pop_back();
+    Node nd{};
+    for (int k = 0; k < 3; ++k) { nd.lo[k] = INFINITY; nd.hi[k] = -INFINITY; }
+    for (int i = j.lo; i < j.hi; ++i)
+      for (int k = 0; k < 3; ++k) {
+        nd.lo[k] = std::min(nd.lo[k], tmin[3 * prim[i] + k]);
+        nd.hi[k] = std::max(nd.hi[k], tmax[3 * prim[i] + k]);
+      }
+    if (j.hi - j.lo <= LEAF) {
+      nd.left = nd.right = -1;
+      nd.start = j.lo;
+      nd.count = j.hi - j.lo;
+      nodes[j.node] = nd;
+      continue;
+    }
+    int axis = 0;
+    for (int k = 1; k < 3; ++k)
+      if (nd.hi[k] - nd.lo[k] > nd.hi[axis] - nd.lo[axis]) axis = k;
+    const int mid = (j.lo + j.hi) / 2;
+    std::nth_element(prim.begin() + j.lo, prim.begin() + mid, prim.begin() + j.hi,
+                     [&](int a, int b) { return cent[3 * a + axis] < cent[3 * b + axis]; });
+    const int lc = (int)nodes.size();
+    nodes.push_back(Node{});
+    const int rc = (int)nodes.size();
+    nodes.push_back(Node{});
+    nd.left = lc;
+    nd.right = rc;
+    nd.start = nd.count = 0;
+    nodes[j.node] = nd;
+    stack.push_back({rc, mid, j.hi});
+    stack.push_back({lc, j.lo, mid});
+  }
+  std::vector<Tri> tris(nf);
+  std::vector<int> tof(nf);
+  for (int64_t k = 0; k < nf; ++k) {
+    const int i = prim[k];
+    Tri T{};
+    for (int c = 0; c < 3; ++c) {
+      T.a[c] = V[3 * Fc[3 * i] + c];
+      T.b[c] = V[3 * Fc[3 * i + 1] + c];
+      T.c[c] = V[3 * Fc[3 * i + 2] + c];
+    }
+    T.face = i;
+    tris[k] = T;
+    tof[i] = (int)k;
+  }
+  (void)nv;
+  CUDA_TRY(f->mesh_nodes.ensure(sizeof(Node) * nodes.size()));
+  CUDA_TRY(f->mesh_tris.ensure(sizeof(Tri) * tris.size()));
+  CUDA_TRY(f->mesh_tof.ensure(sizeof(int) * tof.size()));
+  CUDA_TRY(cudaMemcpy(f->mesh_nodes.p, nodes.data(), sizeof(Node) * nodes.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(f->mesh_tris.p, tris.data(), sizeof(Tri) * tris.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(f->mesh_tof.p, tof.data(), sizeof(int) * tof.size(), cudaMemcpyHostToDevice));
+  f->M.nodes = f->mesh_nodes.as<Node>();
+  f->M.tris = f->mesh_tris.as<Tri>();
+  f->M.tri_of_face = f->mesh_tof.as<int>();
+  f->M.n_faces = (int)nf;
   return DDF_OK;
 }
 
@@ -496,7 +589,9 @@ int ddf_field_destroy(ddf_field_t f) {
   for (auto& im : f->images) umma::free_image(&im);
   Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones,
                  &f->st_o, &f->st_d, &f->st_tacc, &f->st_texit, &f->st_t, &f->st_thr, &f->st_rad,
-                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks, &f->st_u34, &f->st_g3};
+                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks, &f->st_u34, &f->st_g3,
+                 &f->udf_dirs, &f->udf_vals, &f->udf_pts, &f->udf_best, &f->udf_arg, &f->udf_found, &f->udf_list,
+                 &f->udf_seg, &f->udf_state, &f->mesh_nodes, &f->mesh_tris, &f->mesh_tof};
   for (Buf* b : bufs) b->release();
   if (f->F_dev) cudaFree(f->F_dev);
   delete f;
@@ -541,10 +636,16 @@ int ddf_mlp_input_grad(ddf_field_t f, int32_t net, const double* x, int64_t n, d
 
 int ddf_query(ddf_field_t f, const double* pos, const double* dirs, int64_t n, double* t, uint8_t* hit,
               double* pred, int32_t* obj, void* stream) {
-  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (!has_geometry(f)) return fail(DDF_EUSAGE, "field has no network");
   if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
   if (n == 0) return DDF_OK;
   CUDA_TRY(cudaSetDevice(f->device));
+  if (f->F.is_mesh) {
+    mesh::query_kernel<<<(int)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(f->M, pos, dirs, (int)n, t, hit,
+                                                                               pred, obj);
+    CUDA_TRY(cudaGetLastError());
+    return DDF_OK;
+  }
   QueryOp op{};
   op.list = nullptr; op.count = nullptr; op.n = (int)n; op.seg = nullptr;
   op.pos = pos; op.dirs = dirs; op.t = t; op.hit = hit; op.pred_out = pred; op.obj_out = obj;
@@ -554,11 +655,16 @@ int ddf_query(ddf_field_t f, const double* pos, const double* dirs, int64_t n, d
 
 int ddf_trace(ddf_field_t f, const double* origins, const double* dirs, int64_t n, double* t, uint8_t* hit,
               int32_t* obj, void* stream) {
-  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (!has_geometry(f)) return fail(DDF_EUSAGE, "field has no network");
   if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
   if (n == 0) return DDF_OK;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(f->device));
+  if (f->F.is_mesh) {   // trace_batch = query_batch for mesh fields (field.py:170)
+    mesh::query_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(f->M, origins, dirs, (int)n, t, hit, nullptr, obj);
+    CUDA_TRY(cudaGetLastError());
+    return DDF_OK;
+  }
   if (int rc = ensure_small(f)) return rc;
   CUDA_TRY(f->t_acc.ensure(sizeof(double) * n));
   CUDA_TRY(f->t_exit.ensure(sizeof(double) * n));
@@ -577,11 +683,16 @@ int ddf_trace(ddf_field_t f, const double* origins, const double* dirs, int64_t 
 
 int ddf_normal(ddf_field_t f, const double* origins, const double* dirs, const double* t_hit, const int32_t* obj,
                int64_t n, double* normals, uint8_t* valid, void* stream) {
-  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (!has_geometry(f)) return fail(DDF_EUSAGE, "field has no network");
   if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
   if (n == 0) return DDF_OK;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(f->device));
+  if (f->F.is_mesh) {   // re-intersects (field.py:174-176); t_hit and obj are not used
+    mesh::normal_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(f->M, origins, dirs, (int)n, normals, valid);
+    CUDA_TRY(cudaGetLastError());
+    return DDF_OK;
+  }
   if (int rc = ensure_small(f)) return rc;
   NormalOp op{};
   op.o = origins; op.d = dirs; op.t_hit = t_hit; op.backoff = f->F.backoff; op.normals = normals; op.valid = valid;
@@ -602,7 +713,7 @@ int ddf_normal(ddf_field_t f, const double* origins, const double* dirs, const d
 
 int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_config_t* cfg, double* accum,
                     ddf_render_stats_t* stats, void* stream) {
-  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (!has_geometry(f)) return fail(DDF_EUSAGE, "field has no network");
   if (!cam || !cfg || !accum) return fail(DDF_EUSAGE, "null argument");
   if (cfg->bounces < 1) return fail(DDF_EUSAGE, "path mode needs bounces >= 1");   // render.py:207-208
   if (cfg->spp < 1) return fail(DDF_EUSAGE, "spp must be >= 1");                 // render.py:119-120
@@ -715,7 +826,14 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
       f->prof.launches += 1;
     }
     CUDA_TRY(cudaGetLastError());
-    if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st)) return rc;
+    if (f->F.is_mesh) {
+      ProfScope ps(f->prof, Prof::FWD, st);
+      mesh::trace_paths_kernel<<<g, 256, 0, st>>>(f->M, S, nullptr, nullptr, Pw);
+      f->prof.launches += 1;
+      f->prof.fwd_launches += 1;
+    } else if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st)) {
+      return rc;
+    }
     {
       ProfScope ps(f->prof, Prof::OTHER, st);
       after_primary_kernel<<<g, 256, 0, st>>>(w, S, Pw);
@@ -730,17 +848,32 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
       int rc = compact_flags(f, S.alive, f->F.n_obj > 1 ? S.obj : nullptr, Pw, f->F.n_obj, f->list.as<int>(),
                              sm.seg, sm.count2, sm.stats + 1, st);
       if (rc) return rc;
-      GradOutOp op{};
-      op.list = f->list.as<int>(); op.count = sm.count2; op.n = Pw;
-      op.seg = f->F.n_obj > 1 ? sm.seg : nullptr;
-      op.S = S; op.backoff = f->F.backoff;
-      if ((rc = run_mlp(f, f->F, op, Pw, true, st))) return rc;
+      if (f->F.is_mesh) {
+        ProfScope ps(f->prof, Prof::GRAD, st);
+        mesh::face_normal_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->M, S, f->list.as<int>(), sm.count2);
+        f->prof.launches += 1;
+        f->prof.grad_launches += 1;
+      } else {
+        GradOutOp op{};
+        op.list = f->list.as<int>(); op.count = sm.count2; op.n = Pw;
+        op.seg = f->F.n_obj > 1 ? sm.seg : nullptr;
+        op.S = S; op.backoff = f->F.backoff;
+        if ((rc = run_mlp(f, f->F, op, Pw, true, st))) return rc;
+      }
       {
         ProfScope ps(f->prof, Prof::OTHER, st);
         bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->F_dev, w, S, f->list.as<int>(), sm.count2, b);
         f->prof.launches += 1;
       }
-      if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st))) return rc;
+      if (f->F.is_mesh) {
+        ProfScope ps(f->prof, Prof::FWD, st);
+        mesh::trace_paths_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->M, S, f->list.as<int>(), sm.count2,
+                                                                              Pw);
+        f->prof.launches += 1;
+        f->prof.fwd_launches += 1;
+      } else if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st))) {
+        return rc;
+      }
       {
         ProfScope ps(f->prof, Prof::OTHER, st);
         after_bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(w, S, f->list.as<int>(), sm.count2);
@@ -829,6 +962,48 @@ int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, 
   compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, (int)n, 1, g_cs.blocks.as<int>(), list);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
+  return DDF_OK;
+}
+
+int ddf_mesh_create(const double* vertices, int64_t n_vertices, const int32_t* faces, int64_t n_faces,
+                    int32_t device, ddf_field_t* out) {
+  if (!out || !vertices || !faces) return fail(DDF_EUSAGE, "null argument");
+  if (n_vertices < 0 || n_faces < 0 || n_faces > (1ll << 28)) return fail(DDF_EDATA, "bad mesh sizes");
+  if (n_faces == 0) return fail(DDF_EDATA, "cannot build a BVH over an empty mesh");   // mesh.py:98-99
+  for (int64_t i = 0; i < 3 * n_faces; ++i)
+    if (faces[i] < 0 || faces[i] >= n_vertices) return fail(DDF_EDATA, "face index out of range");   // mesh.py:33-34
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = 0; i < n_vertices; ++i)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], vertices[3 * i + k]);
+      hi[k] = std::max(hi[k], vertices[3 * i + k]);
+    }
+  const double b6[6] = {lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]};
+  ddf_field_t h = nullptr;
+  if (int rc = ddf_field_create(1.0, b6, DDF_PREC_FP32, device, &h)) return rc;
+  h->F.is_mesh = 1;
+  if (int rc = build_mesh(h, vertices, n_vertices, faces, n_faces)) {
+    ddf_field_destroy(h);
+    return rc;
+  }
+  cudaError_t e = cudaMemcpy(h->F_dev, &h->F, sizeof(FieldDev), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    ddf_field_destroy(h);
+    return fail(DDF_ECUDA, cudaGetErrorString(e));
+  }
+  *out = h;
+  return DDF_OK;
+}
+
+int ddf_mesh_intersect(ddf_field_t f, const double* origins, const double* dirs, int64_t n, double t_min,
+                       double t_max, int64_t* face, double* t, double* u, double* v, void* stream) {
+  if (!f || !f->F.is_mesh) return fail(DDF_EUSAGE, "not a mesh field");
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad row count");
+  if (n == 0) return DDF_OK;
+  CUDA_TRY(cudaSetDevice(f->device));
+  mesh::intersect_kernel<<<(int)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(f->M, origins, dirs, (int)n, t_min,
+                                                                                 t_max, face, t, u, v);
+  CUDA_TRY(cudaGetLastError());
   return DDF_OK;
 }
 

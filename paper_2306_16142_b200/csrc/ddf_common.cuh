@@ -176,6 +176,7 @@ struct FieldDev {
   double backoff;     // 0.5 delta         (field.py:237)
   int max_steps;      // ceil(diag/step)+4 (field.py:272-273)
   bool composite;
+  int is_mesh;        // 1: exact triangle-mesh field (OracleField), no networks
   NetDev net[DDF_MAX_OBJECTS];
 };
 

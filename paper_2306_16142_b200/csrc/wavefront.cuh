@@ -51,6 +51,13 @@ __device__ __forceinline__ void slot_sp(const WaveDev& w, int p, int& s, int& i)
 
 // slab test + march initialisation for a new ray (field.py:265-269)
 __device__ __forceinline__ void begin_trace(const FieldDev& F, const PathState& S, int p, d3 o, d3 d) {
+  if (F.is_mesh) {   // mesh fields trace every ray exactly (field.py:161-168), no domain box
+    S.march[p] = 1;
+    S.t[p] = INFINITY;
+    S.hit[p] = 0;
+    S.obj[p] = -1;
+    return;
+  }
   double u3, u4;
   dir_u34(d, u3, u4);
   S.u34[2 * p] = u3;

@@ -131,6 +131,7 @@ def main():
     np.savez_compressed(path, **out)
     print("wrote", path, {k: getattr(v, "shape", None) for k, v in out.items()})
     main_udf()
+    main_mesh()
 
 
 def main_udf():
@@ -161,8 +162,56 @@ def main_udf():
     print("wrote", path, {k: getattr(v, "shape", None) for k, v in out.items()})
 
 
+def mesh_rays(n, seed):
+    """Half random rays from a [-2.5, 2.5]^3 shell, half aimed at the origin
+    with jitter; both from default_rng(seed)."""
+    rng = np.random.default_rng(seed)
+    o = rng.uniform(-2.5, 2.5, (n, 3))
+    d = rng.normal(size=(n, 3))
+    half = n // 2
+    d[:half] = -o[:half] + 0.3 * rng.normal(size=(half, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return o, d
+
+
+def main_mesh():
+    """Exact mesh backend: mesh.intersect_rays over the BVH and the linear
+    scan, OracleField query / normal, render_path / render_depth /
+    render_normal with an OracleField backend (field.py:144-200,
+    mesh.py:264-279, render.py:144-247)."""
+    from ddfield import mesh as rmesh
+    from ddfield import meshes
+    out = {}
+    for name, m in (("blob", meshes.blob(3, 0)), ("cube", meshes.cube(0.8)), ("ico", meshes.icosphere(2))):
+        o, d = mesh_rays(2048, {"blob": 1, "cube": 2, "ico": 3}[name])
+        bvh = rmesh.Bvh(m)
+        f, t, u, v = rmesh.intersect_rays(bvh, o, d)
+        fl, tl, ul, vl = rmesh.intersect_rays(m, o, d)
+        assert np.array_equal(f, fl) and np.array_equal(t, tl)
+        out[f"{name}_o"], out[f"{name}_d"] = o, d
+        out[f"{name}_face"], out[f"{name}_t"], out[f"{name}_u"], out[f"{name}_v"] = f, t, u, v
+        fw, tw, _, _ = rmesh.intersect_rays(bvh, o, d, 0.5, 3.0)
+        out[f"{name}_face_win"], out[f"{name}_t_win"] = fw, tw
+        of = field.OracleField(m)
+        out[f"{name}_q_t"], out[f"{name}_q_hit"] = of.query_batch(o, d)
+        out[f"{name}_n"], out[f"{name}_n_valid"] = of.normal_batch(o, d)
+    of = field.OracleField(meshes.blob(3, 0))
+    cam = render.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4.0, width=40, height=30)
+    cfg = render.RenderConfig(mode="path", spp=3, bounces=3, albedo=0.6, env_radiance=1.2, seed=7)
+    out["blob_film"] = render.render(of, cam, cfg).data[:, :, 0]
+    cube = field.OracleField(meshes.cube(0.8))
+    cc = render.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4.0, width=21, height=21)
+    out["cube_depth"] = render.render_depth(cube, cc).data
+    out["cube_normal"] = render.render_normal(cube, cc, render.RenderConfig(mode="normal")).data
+    path = os.path.join(HERE, "reference_golden_mesh.npz")
+    np.savez_compressed(path, **out)
+    print("wrote", path, {k: getattr(v, "shape", None) for k, v in out.items()})
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["udf"]:
         main_udf()
+    elif sys.argv[1:] == ["mesh"]:
+        main_mesh()
     else:
         main()
