@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf", "bvh"])
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
@@ -314,6 +314,103 @@ def bench_udf(args, rank, world, local):
         print(json.dumps(res))
 
 
+# ----------------------------------------------------------------- BVH mesh render
+BVH_MESH = ("blob", 4, 0)     # meshes.blob(4, 0): 5,120 triangles, the reference's bunny-class test mesh
+
+
+def cpu_bvh(args, reference_line=False):
+    """render_path over the exact mesh field on the CPU: the oracle's float64
+    linear scan (BruteForceField semantics) on a bounded band sample."""
+    from oracle import cpu_ddf as O
+    from paper_2306_16142_b200 import configs as C
+    from paper_2306_16142_b200 import meshes as MS
+    m = MS.blob(*BVH_MESH[1:])
+    f = O.MeshField(m.vertices, m.faces)
+    w = C.WORKLOADS["c3"]
+    cam = O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=w["W"], height=w["H"])
+    cfg = O.PathConfig(spp=1, bounces=w["bounces"], albedo=0.7, env=1.0, seed=C.RENDER_SEED)
+    rows = [w["H"] // 2 + k for k in (-64, 0, 64)]
+    O.render_path(f, cam, cfg, pix_range=(rows[0] * w["W"], rows[0] * w["W"] + 16))
+    t0 = time.perf_counter()
+    n = 0
+    for r in rows:
+        O.render_path(f, cam, cfg, pix_range=(r * w["W"], (r + 1) * w["W"]))
+        n += w["W"]
+    s = time.perf_counter() - t0
+    v = n / s
+    desc = f"3 pixel rows x {w['W']} px at spp=1 of the c3 camera, 5,120-triangle blob, float64 linear scan"
+    base = {"value": v, "unit": "path_samples/s", "cores": cpu_cores(), "kind": "port", "sample": desc}
+    if not reference_line:
+        return base
+    return {"impl": "reference", "metric": "path_samples_per_s", "value": v, "unit": "path_samples/s",
+            "n_gpus": args.gpus, "steps": 1, "warmup": 1, "ms_per_step": 1e3 * s, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "bvh", "sample": desc}, "cpu_baseline": base,
+            "e2e": {"value": v, "unit": "path_samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def bench_bvh(args, rank, world, local):
+    """render.render_path with the exact mesh backend (OracleField over a BVH)
+    at config 3's film, spp and bounces: the BVH side of the paper's
+    DDF-vs-BVH render timing (Fig. 5)."""
+    import torch
+    from paper_2306_16142_b200 import configs as C
+    from paper_2306_16142_b200 import meshes as MS
+    from paper_2306_16142_b200 import render as R
+    from paper_2306_16142_b200.mesh import CudaMeshField
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    m = MS.blob(*BVH_MESH[1:])
+    fld = CudaMeshField(m)
+    cam = C.camera("c3")
+    cfg = C.render_config("c3")
+    n_pix = cam.width * cam.height
+    accum = torch.empty(n_pix, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(max(3, args.warmup)):
+        R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, st = R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.mean(times))
+    cfg.profile = 1
+    _, prof = R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
+    cfg.profile = 0
+    te = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        R.render_path(fld, cam, cfg)
+        te.append(time.perf_counter() - t0)
+    samples = n_pix * cfg.spp
+    res = {"metric": "path_samples_per_s", "value": samples / (ms / 1e3), "unit": "path_samples/s", "n_gpus": world,
+           "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "bvh", "mesh": "blob(4, 0)", "triangles": int(m.n_faces), "W": cam.width,
+                      "H": cam.height, "spp": cfg.spp, "bounces": cfg.bounces,
+                      "l2": "flushed (256 MB write) between timed steps"},
+           "roofline": {"bound": "fp64", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
+                        "kernel": "BVH traversal (f64 Moller-Trumbore, one thread per ray)",
+                        "trace_ms": prof["ms_forward"], "normal_ms": prof["ms_gradient"],
+                        "compaction_ms": prof["ms_compact"], "other_ms": prof["ms_other"]},
+           "cpu_baseline": cpu_bvh(args) if args.cpu_baseline else None,
+           "e2e": {"value": samples / float(np.mean(te)), "unit": "path_samples/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 8 * n_pix},
+           "gpu_launches": int(st["kernel_launches"]) * args.steps, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(res))
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -375,6 +472,10 @@ def main():
             return
         print(json.dumps(cpu_queries(args, reference_line=True)))
         return
+    if args.impl == "reference" and name == "bvh":
+        if rank == 0:
+            print(json.dumps(cpu_bvh(args, reference_line=True)))
+        return
     if args.impl == "reference" and name == "udf":
         if rank == 0:
             print(json.dumps(cpu_udf(args, reference_line=True)))
@@ -414,6 +515,8 @@ def main():
         return bench_queries(args, rank, world, local)
     if name == "udf":
         return bench_udf(args, rank, world, local)
+    if name == "bvh":
+        return bench_bvh(args, rank, world, local)
 
     dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
