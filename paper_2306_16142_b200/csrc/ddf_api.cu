@@ -138,7 +138,7 @@ int max_width(const FieldDev& F) {
 // ---------------------------------------------------------------- engine dispatch
 template <int M, int KMAX>
 size_t simt_smem() {
-  return sizeof(double) * M * 8 + sizeof(float) * (2 * KMAX * M + simt::KC * simt::NC + 2 * M) +
+  return sizeof(double) * M * 8 + sizeof(float) * (2 * KMAX * M + 2 * simt::KC * simt::NC + 2 * M) +
          sizeof(uint32_t) * DDF_MAX_LAYERS * KMAX * (M / 32) + sizeof(int) * 2 * M;
 }
 

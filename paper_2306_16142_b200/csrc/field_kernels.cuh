@@ -205,7 +205,7 @@ struct Tile {
     t.best = reinterpret_cast<double*>(p); p += sizeof(double) * M * 3;
     t.actA = reinterpret_cast<float*>(p); p += sizeof(float) * KMAX * M;
     t.actB = reinterpret_cast<float*>(p); p += sizeof(float) * KMAX * M;
-    t.ws = reinterpret_cast<float*>(p); p += sizeof(float) * KC * NC;
+    t.ws = reinterpret_cast<float*>(p); p += sizeof(float) * 2 * KC * NC;   // double-buffered weight chunks
     t.head = reinterpret_cast<float*>(p); p += sizeof(float) * M * 2;
     t.mask = reinterpret_cast<uint32_t*>(p); p += sizeof(uint32_t) * DDF_MAX_LAYERS * KMAX * (M / 32);
     t.bobj = reinterpret_cast<int*>(p); p += sizeof(int) * M;

@@ -3,8 +3,8 @@
 // Restates ddfield/neural.py:138-157 (forward_batch) and :229-249
 // (input_gradient_batch) for one tile of M rows held in shared memory:
 // activations live transposed as act[k][m] (rows contiguous), weight K-chunks
-// stream from L2 into a [KC][NC] staging buffer, each thread owns an
-// RM x 8 register tile.  Hidden-layer ReLU masks for the gradient are kept as
+// stream from L2 into double-buffered [KC][NC] stages (cp.async), each thread owns an
+// 8 x 8 (or 8 x 4) register tile.  Hidden-layer ReLU masks for the gradient are kept as
 // bit words in shared memory (mask[l][n][m/32]).
 //
 // Exact fp32 arithmetic (no TF32): SURVEY App. B measured max|d|/rms <= 1e-5
@@ -16,96 +16,142 @@ namespace ddf {
 namespace simt {
 
 constexpr int NT = 256;          // threads per CTA
-constexpr int TX = 16, TY = 16;  // thread grid over (cols, rows)
 constexpr int KC = 32;           // K chunk staged per step
-constexpr int NC = 128;          // N chunk (two groups of 64 columns)
+constexpr int NC = 256;          // N chunk of a weight stage
 
 template <int M, int KMAX>
 struct Smem {
-  static constexpr int RM = M / TY;
   static constexpr int ACT = KMAX * M;                  // floats per activation buffer
   static constexpr int MASK_WORDS = (DDF_MAX_LAYERS) * KMAX * (M / 32);
   static constexpr size_t bytes =
-      sizeof(float) * (2 * ACT + KC * NC + M * 2) + sizeof(uint32_t) * MASK_WORDS +
+      sizeof(float) * (2 * ACT + 2 * KC * NC + M * 2) + sizeof(uint32_t) * MASK_WORDS +
       sizeof(double) * M * 8 + sizeof(int) * M * 2;
 };
 
 enum EpiMode : int { EPI_RELU = 0, EPI_RELU_MASK = 1, EPI_MASKMUL = 2, EPI_LINEAR = 3 };
 
+// Weight K-chunk [kc][NC] of columns [n0, n0 + nc) -> shared memory with
+// cp.async (16 B per copy; columns >= nc are zero-filled).
+template <int NCT>
+__device__ __forceinline__ void stage_weights(const float* __restrict__ Wkn, int N, int k0, int kc, int n0, int nc,
+                                              float* dst) {
+  for (int i = threadIdx.x; i < kc * (NCT / 4); i += NT) {
+    const int k = i / (NCT / 4), q = i % (NCT / 4);
+    const bool in = q * 4 < nc;
+    const float* src = in ? Wkn + (size_t)(k0 + k) * N + n0 + q * 4 : Wkn;
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + k * NCT + q * 4);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(in ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // out[n][m] = epi( sum_k in[k][m] * Wkn[k][n] (+ bias[n]) )
 // Wkn: [K][N] row-major in global memory (K, N multiples of 16).
-template <int M>
-__device__ __forceinline__ void gemm_layer(const float* __restrict__ Wkn, const float* __restrict__ bias,
-                                           int K, int N, const float* act_in, float* act_out, float* ws,
-                                           int mode, uint32_t* mask_out, const uint32_t* mask_in) {
-  constexpr int RM = M / TY;
-  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-  for (int n0 = 0; n0 < N; n0 += NC) {
-    const int nc = min(NC, N - n0);
-    float acc[RM][8];
+// Register tile 8 rows x RN columns per thread: tx = tid % TXM owns rows
+// [8 tx, 8 tx + 8), ty = tid / TXM owns columns {4 ty + j} (+ 128 for the
+// second four when RN = 8) of each 256-column chunk -- 64 FFMA per four
+// 16-byte shared loads at M = 64.  Weight chunks are double-buffered with
+// cp.async and each k step's operands are loaded one step ahead.
+template <int M, int NCT>
+__device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const float* __restrict__ bias,
+                                            int K, int N, const float* act_in, float* act_out, float* ws,
+                                            int mode, uint32_t* mask_out, const uint32_t* mask_in) {
+  constexpr int RM = 8, TXM = M / RM, TYN = NT / TXM, RN = NCT / TYN;
+  static_assert(RN == 4 || RN == 8, "register tile");
+  const int tid = threadIdx.x, tx = tid % TXM, ty = tid / TXM;
+  const int m0 = tx * RM;
+  const int nk = (K + KC - 1) / KC;
+  auto col = [&](int j) { return RN == 8 ? (j < 4 ? ty * 4 + j : NCT / 2 + ty * 4 + (j - 4)) : ty * 4 + j; };
+  for (int n0 = 0; n0 < N; n0 += NCT) {
+    const int nc = min(NCT, N - n0);
+    float acc[RM][RN];
 #pragma unroll
     for (int i = 0; i < RM; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-    for (int k0 = 0; k0 < K; k0 += KC) {
-      const int kc = min(KC, K - k0);
-      __syncthreads();
-      for (int i = tid; i < kc * (NC / 4); i += NT) {
-        const int k = i / (NC / 4), q = i % (NC / 4);
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (q * 4 < nc) v = __ldg(reinterpret_cast<const float4*>(Wkn + (size_t)(k0 + k) * N + n0 + q * 4));
-        *reinterpret_cast<float4*>(ws + k * NC + q * 4) = v;
+      for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
+    stage_weights<NCT>(Wkn, N, 0, min(KC, K), n0, nc, ws);
+    for (int c = 0; c < nk; ++c) {
+      const int k0 = c * KC, kc = min(KC, K - k0);
+      if (c + 1 < nk) {
+        stage_weights<NCT>(Wkn, N, k0 + KC, min(KC, K - k0 - KC), n0, nc, ws + ((c + 1) & 1) * KC * NCT);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncthreads();
+      const float* wsc = ws + (c & 1) * KC * NCT + ty * 4;
+      const float* ai = act_in + (size_t)k0 * M + m0;
+      float4 a0 = *reinterpret_cast<const float4*>(ai), a1 = *reinterpret_cast<const float4*>(ai + 4);
+      float4 w0 = *reinterpret_cast<const float4*>(wsc), w1 = w0;
+      if constexpr (RN == 8) w1 = *reinterpret_cast<const float4*>(wsc + NCT / 2);
 #pragma unroll 4
       for (int k = 0; k < kc; ++k) {
-        float a[RM];
-        if constexpr (RM == 4) {
-          float4 t = *reinterpret_cast<const float4*>(act_in + (k0 + k) * M + ty * 4);
-          a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
-        } else {
-          float2 t = *reinterpret_cast<const float2*>(act_in + (k0 + k) * M + ty * 2);
-          a[0] = t.x; a[1] = t.y;
-        }
-        const float4 w0 = *reinterpret_cast<const float4*>(ws + k * NC + tx * 4);
-        const float4 w1 = *reinterpret_cast<const float4*>(ws + k * NC + 64 + tx * 4);
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        if (k + 1 < kc) {   // operands of step k + 1 in flight while step k computes
+          a0 = *reinterpret_cast<const float4*>(ai + (k + 1) * M);
+          a1 = *reinterpret_cast<const float4*>(ai + (k + 1) * M + 4);
+          w0 = *reinterpret_cast<const float4*>(wsc + (k + 1) * NCT);
+          if constexpr (RN == 8) w1 = *reinterpret_cast<const float4*>(wsc + (k + 1) * NCT + NCT / 2);
+        }
 #pragma unroll
         for (int i = 0; i < RM; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+          for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
       }
+      __syncthreads();   // this buffer is refilled two chunks later
     }
-    // epilogue
+    // epilogue: a thread's 8 rows of one column are contiguous -> two vector stores
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-      if (c >= nc) continue;
-      const int n = n0 + c;
-      const float bn = (bias != nullptr) ? __ldg(bias + n) : 0.f;
+    for (int j = 0; j < RN; ++j) {
+      const int cc = col(j);
+      const bool live = cc < nc;
+      const int n = n0 + (live ? cc : 0);
+      const float bn = (live && bias != nullptr) ? __ldg(bias + n) : 0.f;
+      float v[RM];
       uint32_t bits = 0;
+      const uint32_t mw = (mode == EPI_MASKMUL && live) ? mask_in[n * (M / 32) + (m0 >> 5)] >> (m0 & 31) : 0u;
 #pragma unroll
       for (int i = 0; i < RM; ++i) {
-        const int m = ty * RM + i;
-        float v = acc[i][j];
+        float x = acc[i][j];
         if (mode == EPI_RELU || mode == EPI_RELU_MASK) {
-          v = v + bn;
-          const bool on = v > 0.f;
-          v = on ? v : 0.f;
+          x = x + bn;
+          const bool on = x > 0.f;
+          x = on ? x : 0.f;
           bits |= (on ? 1u : 0u) << i;
         } else if (mode == EPI_MASKMUL) {
-          const uint32_t w = mask_in[n * (M / 32) + (m >> 5)];
-          v = ((w >> (m & 31)) & 1u) ? v : 0.f;
+          x = ((mw >> i) & 1u) ? x : 0.f;
         }
-        act_out[n * M + m] = v;
+        v[i] = x;
       }
-      if (mode == EPI_RELU_MASK && bits) {
-        const int m0 = ty * RM;
-        atomicOr(&mask_out[n * (M / 32) + (m0 >> 5)], bits << (m0 & 31));
+      if (live) {
+        *reinterpret_cast<float4*>(act_out + n * M + m0) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(act_out + n * M + m0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      }
+      if (mode == EPI_RELU_MASK) {
+        // OR the four lanes that share one 32-row mask word (aligned lane groups)
+        uint32_t word = bits << (m0 & 31);
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        if (live && (tx & 3) == 0) mask_out[n * (M / 32) + (m0 >> 5)] = word;
       }
     }
   }
   __syncthreads();
+}
+
+// 128-column chunks for layers at most 128 wide (no idle columns), 256 otherwise
+template <int M>
+__device__ __forceinline__ void gemm_layer(const float* __restrict__ Wkn, const float* __restrict__ bias,
+                                           int K, int N, const float* act_in, float* act_out, float* ws,
+                                           int mode, uint32_t* mask_out, const uint32_t* mask_in) {
+  if constexpr (M == 64) {
+    if (N <= 128) {
+      gemm_chunks<M, 128>(Wkn, bias, K, N, act_in, act_out, ws, mode, mask_out, mask_in);
+      return;
+    }
+  }
+  gemm_chunks<M, NC>(Wkn, bias, K, N, act_in, act_out, ws, mode, mask_out, mask_in);
 }
 
 // Head (identity, N = 1): out[m] = sum_k act[k][m] * w[k] + b  (fp32).
