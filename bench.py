@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf", "bvh"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf", "bvh", "march"])
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
@@ -53,7 +53,7 @@ def oracle_field(name):
     if w.get("scene"):
         centers, scale, albedos = C.scene_layout()
         return O.Field(nets, C.CFG_DELTA, bounds=C.SCENE_BOX, centers=centers, scale=scale, albedos=albedos)
-    return O.Field(nets, C.CFG_DELTA, bounds=C.UNIT_BOX)
+    return O.Field(nets, C.delta(name), bounds=C.UNIT_BOX)
 
 
 def cpu_sample_bands(name):
@@ -64,7 +64,7 @@ def cpu_sample_bands(name):
     W, H = w["W"], w["H"]
     if name == "c2":
         return [(0, W * H)], w["spp"], "full render (128x128, 4 spp)"
-    rows_total = {"c3": 32, "c4": 8, "c5": 16}[name]
+    rows_total = {"c3": 32, "c4": 8, "c5": 16, "march": 8}[name]
     nb = 8
     per = max(1, rows_total // nb)
     bands = []

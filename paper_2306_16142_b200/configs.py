@@ -13,6 +13,10 @@ Kaiming-uniform weights with zero biases from the stated seed.
   c5  render 1024x1024, 32 spp, 6 bounces, 8 x (65->6x256->1) seeds 10-17 at
       (+-0.75)^3, scale 0.5, albedos U[0.2, 0.9] from default_rng(5), bounds
       [-1.25, 1.25]^3, bf16
+  march the trained-checkpoint regime: c3's network,
+      film and camera at 4 spp, 2 bounces, with delta = 0.1 (the reference
+      default) and the head scaled (g * 0.05, b + 0.12) so predictions
+      straddle the 0.098 hit threshold -- rays sphere-march up to 43 steps
 """
 
 from __future__ import annotations
@@ -38,6 +42,8 @@ WORKLOADS = {
                rr_start=3, tile=64, precision="bf16"),
     "c5": dict(kind="render", widths=(65,) + (256,) * 6 + (1,), net_seed=None, W=1024, H=1024, spp=32, bounces=6,
                scene=True, precision="bf16"),
+    "march": dict(kind="render", widths=(65,) + (512,) * 8 + (1,), net_seed=2, W=512, H=512, spp=4, bounces=2,
+                  precision="bf16", delta=0.1, march_head=(0.05, 0.12)),
 }
 
 
@@ -57,7 +63,16 @@ def models(name):
     w = WORKLOADS[name]
     if w.get("scene"):
         return [kaiming_uniform(w["widths"], s) for s in range(10, 18)]
-    return [kaiming_uniform(w["widths"], w["net_seed"])]
+    m = kaiming_uniform(w["widths"], w["net_seed"])
+    if "march_head" in w:
+        gs, bs = w["march_head"]
+        m.g[-1] = m.g[-1] * gs
+        m.b[-1] = m.b[-1] + bs
+    return [m]
+
+
+def delta(name) -> float:
+    return WORKLOADS[name].get("delta", CFG_DELTA)
 
 
 def query_rays(n: int, seed: int = 0):
@@ -95,4 +110,4 @@ def build_field(name, precision: str | None = None):
     if w.get("scene"):
         centers, scale, albedos = scene_layout()
         return CudaNeuralField.scene(ms, centers, scale, albedos, CFG_DELTA, bounds=SCENE_BOX, precision=prec)
-    return CudaNeuralField(ms[0], CFG_DELTA, bounds=UNIT_BOX, precision=prec)
+    return CudaNeuralField(ms[0], delta(name), bounds=UNIT_BOX, precision=prec)
