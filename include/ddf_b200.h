@@ -136,12 +136,18 @@ int ddf_mesh_create(const double* vertices, int64_t n_vertices, const int32_t* f
 int ddf_mesh_intersect(ddf_field_t f, const double* origins, const double* dirs, int64_t n, double t_min,
                        double t_max, int64_t* face, double* t, double* u, double* v, void* stream);
 
+/* mesh.closest_distance (mesh.py:324-330) == _kernels.closest_dist_batch
+   (_kernels.py:451-509): exact distance from each point (device (n,3) f64) to
+   the mesh surface -> out (n,) f64.  OracleField.exact_distance. */
+int ddf_mesh_closest(ddf_field_t f, const double* points, int64_t n, double* out, void* stream);
+
 /* field.udf_many (field.py:418-488) for a neural backend: unsigned distance
    at n points (device (n,3) f64) = min over the n_dirs Halton sphere
    directions (field.py:126-141) of query_batch's t (+inf on a miss), then,
    when polish != 0, two rounds of golden-section search per angle
    (field.py:450-487).  out (n,) f64 device; +inf where every direction misses.
-   n_dirs >= 1. */
+   n_dirs >= 1.  On a mesh handle (an exact backend) this is the exact
+   closest-point distance, as udf_many's exact shortcut (field.py:431-433). */
 int ddf_udf(ddf_field_t f, const double* points, int64_t n, int32_t n_dirs, int32_t polish, double* out,
             void* stream);
 /* recon.udf_grid (recon.py:61-81): ddf_udf at the resolution^3 vertices of

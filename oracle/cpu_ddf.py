@@ -832,3 +832,65 @@ class MeshField:
             nn[dots > 0.0] *= -1.0
             n[valid] = nn
         return n, valid
+
+
+def point_tri_dist_sq(p, a, b, c):
+    """_kernels.py:363-424 (Ericson's closest-point region tests) elementwise
+    over broadcast arrays, the first matching region in the reference's order."""
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ab, ac, ap = b - a, c - a, p - a
+        dot = lambda u, v: u[..., 0] * v[..., 0] + u[..., 1] * v[..., 1] + u[..., 2] * v[..., 2]  # noqa: E731
+        d1, d2 = dot(ab, ap), dot(ac, ap)
+        bp = p - b
+        d3, d4 = dot(ab, bp), dot(ac, bp)
+        vc = d1 * d4 - d3 * d2
+        cp = p - c
+        d5, d6 = dot(ab, cp), dot(ac, cp)
+        vb = d5 * d2 - d1 * d6
+        va = d3 * d6 - d5 * d4
+        e1, e2 = d4 - d3, d5 - d6
+
+        def frac(num, den):
+            return np.where(den != 0.0, num / np.where(den != 0.0, den, 1.0), 0.0)
+
+        w_ab = frac(d1, d1 - d3)[..., None]
+        w_ac = frac(d2, d2 - d6)[..., None]
+        w_bc = frac(e1, e1 + e2)[..., None]
+        denom = va + vb + vc
+        v_in = vb / np.where(denom == 0.0, 1.0, denom)
+        w_in = vc / np.where(denom == 0.0, 1.0, denom)
+        cands = [
+            (d1 <= 0.0) & (d2 <= 0.0), dot(ap, ap),
+            (d3 >= 0.0) & (d4 <= d3), dot(bp, bp),
+            (vc <= 0.0) & (d1 >= 0.0) & (d3 <= 0.0), None,
+            (d6 >= 0.0) & (d5 <= d6), dot(cp, cp),
+            (vb <= 0.0) & (d2 >= 0.0) & (d6 <= 0.0), None,
+            (va <= 0.0) & (e1 >= 0.0) & (e2 >= 0.0), None,
+            denom == 0.0, dot(ap, ap),
+        ]
+        e = ap - w_ab * ab
+        cands[5] = dot(e, e)
+        e = ap - w_ac * ac
+        cands[9] = dot(e, e)
+        e = bp - w_bc * (c - b)
+        cands[11] = dot(e, e)
+        e = ap - v_in[..., None] * ab - w_in[..., None] * ac
+        out = dot(e, e)
+        for k in range(len(cands) - 2, -1, -2):
+            out = np.where(cands[k], cands[k + 1], out)
+    return out
+
+
+def _mesh_closest(self, points):
+    """mesh.closest_distance (mesh.py:324-330) by a linear scan
+    (_kernels.linear_closest_batch, _kernels.py:512-531)."""
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    out = np.empty(len(pts))
+    step = max(1, self._chunk // max(len(self.faces), 1))
+    for s in range(0, len(pts), step):
+        d = point_tri_dist_sq(pts[s:s + step, None, :], self._a[None], self._b[None], self._c[None])
+        out[s:s + step] = np.sqrt(d.min(axis=1))
+    return out
+
+
+MeshField.exact_distance = _mesh_closest

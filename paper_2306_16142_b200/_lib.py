@@ -29,7 +29,7 @@ ENC_RAW5, ENC_PE6 = 0, 1
 
 EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "ddf_field_set_precision",
            "ddf_last_error", "ddf_mlp_forward", "ddf_mlp_input_grad", "ddf_query", "ddf_trace",
-           "ddf_normal", "ddf_render_path", "ddf_mesh_create", "ddf_mesh_intersect", "ddf_udf", "ddf_udf_grid", "ddf_rng_doubles", "ddf_compact",
+           "ddf_normal", "ddf_render_path", "ddf_mesh_create", "ddf_mesh_intersect", "ddf_mesh_closest", "ddf_udf", "ddf_udf_grid", "ddf_rng_doubles", "ddf_compact",
            "ddf_debug_counters")
 
 
@@ -109,6 +109,7 @@ def lib():
     L.ddf_compact.argtypes = [dp, i64, dp, dp, vp]
     L.ddf_udf.argtypes = [vp, dp, i64, i32, i32, dp, vp]
     L.ddf_mesh_create.argtypes = [vp, i64, vp, i64, i32, ctypes.POINTER(vp)]
+    L.ddf_mesh_closest.argtypes = [vp, dp, i64, dp, vp]
     L.ddf_mesh_intersect.argtypes = [vp, dp, dp, i64, ctypes.c_double, ctypes.c_double, dp, dp, dp, dp, vp]
     L.ddf_udf_grid.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32, i32, i32, dp, vp]
     L.ddf_debug_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), i32]

@@ -1007,8 +1007,19 @@ int ddf_mesh_intersect(ddf_field_t f, const double* origins, const double* dirs,
   return DDF_OK;
 }
 
+int ddf_mesh_closest(ddf_field_t f, const double* points, int64_t n, double* out, void* stream) {
+  if (!f || !f->F.is_mesh) return fail(DDF_EUSAGE, "not a mesh field");
+  if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad point count");
+  if (n == 0) return DDF_OK;
+  CUDA_TRY(cudaSetDevice(f->device));
+  mesh::closest_kernel<<<(int)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(f->M, points, (int)n, out);
+  CUDA_TRY(cudaGetLastError());
+  return DDF_OK;
+}
+
 int ddf_udf(ddf_field_t f, const double* points, int64_t n, int32_t n_dirs, int32_t polish, double* out,
             void* stream) {
+  if (f && f->F.is_mesh) return ddf_mesh_closest(f, points, n, out, stream);   // exact backends (field.py:431-433)
   if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
   CUDA_TRY(cudaSetDevice(f->device));
   return udf_run(f, points, n, n_dirs, polish != 0, out, (cudaStream_t)stream);
@@ -1016,7 +1027,7 @@ int ddf_udf(ddf_field_t f, const double* points, int64_t n, int32_t n_dirs, int3
 
 int ddf_udf_grid(ddf_field_t f, const double bbox[6], int32_t resolution, int32_t n_dirs, int32_t polish,
                  double* out, void* stream) {
-  if (!f || f->F.n_obj == 0) return fail(DDF_EUSAGE, "field has no network");
+  if (!has_geometry(f)) return fail(DDF_EUSAGE, "field has no network");
   if (!bbox) return fail(DDF_EUSAGE, "null bbox");
   if (resolution < 8) return fail(DDF_EUSAGE, "resolution must be >= 8");   // recon.py:66-67
   if (resolution > 1024) return fail(DDF_EUSAGE, "resolution too large");
@@ -1027,6 +1038,7 @@ int ddf_udf_grid(ddf_field_t f, const double bbox[6], int32_t resolution, int32_
   udf::grid_points_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
       f->udf_pts.as<double>(), resolution, bbox[0], bbox[1], bbox[2], bbox[3], bbox[4], bbox[5]);
   CUDA_TRY(cudaGetLastError());
+  if (f->F.is_mesh) return ddf_mesh_closest(f, f->udf_pts.as<double>(), n, out, st);   // recon.py:61-81, exact
   return udf_run(f, f->udf_pts.as<double>(), n, n_dirs, polish != 0, out, st);
 }
 

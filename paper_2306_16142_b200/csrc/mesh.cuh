@@ -232,5 +232,116 @@ __global__ void face_normal_kernel(const MeshDev M, const PathState S, const int
   }
 }
 
+// ------------------------------------------------------------ closest point
+// _kernels.py:363-424 _point_tri_dist_sq (Ericson's region tests), same
+// operation order; squared distance from p to triangle T.
+__device__ __forceinline__ double point_tri_dist_sq(d3 p, const Tri& T) {
+  const double ax = T.a[0], ay = T.a[1], az = T.a[2];
+  const double bx = T.b[0], by = T.b[1], bz = T.b[2];
+  const double cx = T.c[0], cy = T.c[1], cz = T.c[2];
+  auto dot = [](double x0, double y0, double z0, double x1, double y1, double z1) {
+    return dadd(dadd(dmul(x0, x1), dmul(y0, y1)), dmul(z0, z1));
+  };
+  const double abx = dsub(bx, ax), aby = dsub(by, ay), abz = dsub(bz, az);
+  const double acx = dsub(cx, ax), acy = dsub(cy, ay), acz = dsub(cz, az);
+  const double apx = dsub(p.x, ax), apy = dsub(p.y, ay), apz = dsub(p.z, az);
+  const double d1 = dot(abx, aby, abz, apx, apy, apz);
+  const double d2 = dot(acx, acy, acz, apx, apy, apz);
+  if (d1 <= 0.0 && d2 <= 0.0) return dot(apx, apy, apz, apx, apy, apz);
+  const double bpx = dsub(p.x, bx), bpy = dsub(p.y, by), bpz = dsub(p.z, bz);
+  const double d3 = dot(abx, aby, abz, bpx, bpy, bpz);
+  const double d4 = dot(acx, acy, acz, bpx, bpy, bpz);
+  if (d3 >= 0.0 && d4 <= d3) return dot(bpx, bpy, bpz, bpx, bpy, bpz);
+  const double vc = dsub(dmul(d1, d4), dmul(d3, d2));
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+    const double den = dsub(d1, d3);
+    const double w = den != 0.0 ? ddiv(d1, den) : 0.0;
+    const double ex = dsub(apx, dmul(w, abx)), ey = dsub(apy, dmul(w, aby)), ez = dsub(apz, dmul(w, abz));
+    return dot(ex, ey, ez, ex, ey, ez);
+  }
+  const double cpx = dsub(p.x, cx), cpy = dsub(p.y, cy), cpz = dsub(p.z, cz);
+  const double d5 = dot(abx, aby, abz, cpx, cpy, cpz);
+  const double d6 = dot(acx, acy, acz, cpx, cpy, cpz);
+  if (d6 >= 0.0 && d5 <= d6) return dot(cpx, cpy, cpz, cpx, cpy, cpz);
+  const double vb = dsub(dmul(d5, d2), dmul(d1, d6));
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+    const double den = dsub(d2, d6);
+    const double w = den != 0.0 ? ddiv(d2, den) : 0.0;
+    const double ex = dsub(apx, dmul(w, acx)), ey = dsub(apy, dmul(w, acy)), ez = dsub(apz, dmul(w, acz));
+    return dot(ex, ey, ez, ex, ey, ez);
+  }
+  const double va = dsub(dmul(d3, d6), dmul(d5, d4));
+  const double e1 = dsub(d4, d3), e2 = dsub(d5, d6);
+  if (va <= 0.0 && e1 >= 0.0 && e2 >= 0.0) {
+    const double den = dadd(e1, e2);
+    const double w = den != 0.0 ? ddiv(e1, den) : 0.0;
+    const double ex = dsub(bpx, dmul(w, dsub(cx, bx)));
+    const double ey = dsub(bpy, dmul(w, dsub(cy, by)));
+    const double ez = dsub(bpz, dmul(w, dsub(cz, bz)));
+    return dot(ex, ey, ez, ex, ey, ez);
+  }
+  const double denom = dadd(dadd(va, vb), vc);
+  if (denom == 0.0) return dot(apx, apy, apz, apx, apy, apz);
+  const double v = ddiv(vb, denom), w = ddiv(vc, denom);
+  const double ex = dsub(dsub(apx, dmul(v, abx)), dmul(w, acx));
+  const double ey = dsub(dsub(apy, dmul(v, aby)), dmul(w, acy));
+  const double ez = dsub(dsub(apz, dmul(v, abz)), dmul(w, acz));
+  return dot(ex, ey, ez, ex, ey, ez);
+}
+
+// _kernels.py:427-448
+__device__ __forceinline__ double box_dist_sq(d3 p, const double* lo, const double* hi) {
+  double d = 0.0;
+  const double pc[3] = {p.x, p.y, p.z};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (pc[k] < lo[k]) {
+      const double e = dsub(lo[k], pc[k]);
+      d = dadd(d, dmul(e, e));
+    } else if (pc[k] > hi[k]) {
+      const double e = dsub(pc[k], hi[k]);
+      d = dadd(d, dmul(e, e));
+    }
+  }
+  return d;
+}
+
+// _kernels.py:451-500 closest_dist: exact point-to-surface distance; the
+// minimum over triangles does not depend on the tree
+__device__ __forceinline__ double closest(const MeshDev& M, d3 p) {
+  double best = INFINITY;
+  int stack[STACK];
+  int sp = 0;
+  stack[sp++] = 0;
+  while (sp > 0) {
+    const int node = stack[--sp];
+    double lo[3], hi[3];
+    int4 ln;
+    load_node(M.nodes, node, lo, hi, ln);
+    if (box_dist_sq(p, lo, hi) >= best) continue;
+    if (ln.x < 0) {
+      for (int k = ln.z; k < ln.z + ln.w; ++k) {
+        const double dd = point_tri_dist_sq(p, M.tris[k]);
+        if (dd < best) best = dd;
+      }
+    } else {
+      double llo[3], lhi[3], rlo[3], rhi[3];
+      int4 dummy;
+      load_node(M.nodes, ln.x, llo, lhi, dummy);
+      load_node(M.nodes, ln.y, rlo, rhi, dummy);
+      const double dl = box_dist_sq(p, llo, lhi), dr = box_dist_sq(p, rlo, rhi);
+      if (sp + 2 > STACK) continue;
+      if (dl <= dr) { stack[sp++] = ln.y; stack[sp++] = ln.x; }
+      else { stack[sp++] = ln.x; stack[sp++] = ln.y; }
+    }
+  }
+  return sqrt(best);
+}
+
+__global__ void closest_kernel(const MeshDev M, const double* pts, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = closest(M, ld3(pts, i));
+}
+
 }  // namespace mesh
 }  // namespace ddf

@@ -215,7 +215,14 @@ class CudaMeshField:
         return nr.cpu().numpy(), valid.cpu().numpy().astype(bool)
 
     def exact_distance(self, points):
-        raise NotImplementedError("closest-point distance (mesh.closest_distance) is not on the GPU yet")
+        """OracleField.exact_distance (field.py:198-200) = mesh.closest_distance
+        (mesh.py:324-330): exact point-to-surface distance."""
+        p = np.atleast_2d(np.asarray(points, dtype=np.float64))
+        out = torch.empty(len(p), dtype=torch.float64, device=self.torch_device)
+        if len(p):
+            pd = _dev(p, device=self.torch_device)
+            _lib.check(_lib.lib().ddf_mesh_closest(self._h, _ptr(pd), len(p), _ptr(out), _stream()))
+        return out.cpu().numpy()
 
 
 OracleField = CudaMeshField

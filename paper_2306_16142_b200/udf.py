@@ -10,8 +10,8 @@ results and errors:
 
 The whole computation (direction scan, first argmin, golden-section polish)
 runs on the device through ``ddf_udf`` / ``ddf_udf_grid``; there is no host
-fallback.  Neural backends only: the reference's exact shortcut
-(``backend.exact_distance``) belongs to its mesh backends.
+fallback.  Exact backends (the mesh field, ``exact_udf = True``) take the
+reference's shortcut to the closest-point distance, also on the device.
 """
 
 from __future__ import annotations
@@ -60,11 +60,12 @@ def grid_points(bbox, resolution: int) -> np.ndarray:
     return np.stack([c.ravel() for c in g], axis=1)
 
 
-def _check_exact(backend, exact):
-    if exact is None:
-        exact = getattr(backend, "exact_udf", False)
-    if exact:
-        raise ValueError("exact UDF needs a mesh backend (exact_distance); this backend is neural")
+def _exact(backend, exact) -> bool:
+    """field.py:428-433: exact backends (meshes) shortcut to closest-point distances."""
+    ex = bool(getattr(backend, "exact_udf", False) if exact is None else exact)
+    if not ex and getattr(backend, "exact_udf", False):
+        raise ValueError("the sampled UDF over a mesh backend is not on the GPU; use exact=True")
+    return ex
 
 
 def udf_many_device(backend, points, n_dirs: int = 512, polish: bool = True, out=None, stream=None):
@@ -81,8 +82,9 @@ def udf_many(backend, points, n_dirs: int = 512, exact: bool | None = None, poli
              chunk: int = 250_000) -> np.ndarray:
     """field.py:418-488: (P, 3) points -> (P,) distances, +inf = all directions miss.
     ``chunk`` is accepted for signature parity; the device chunks by itself."""
-    _check_exact(backend, exact)
     pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    if _exact(backend, exact):
+        return backend.exact_distance(pts)
     if len(pts) == 0:
         return np.empty(0)
     d = _dev(pts, device=backend.torch_device)
@@ -104,8 +106,9 @@ def udf_grid(backend, resolution: int = 64, n_dirs: int = 512, bounds=None, exac
     ``bounds`` (default ``backend.grid_bounds``)."""
     if resolution < 8:
         raise ValueError("resolution must be >= 8")
-    _check_exact(backend, exact)
     box = np.asarray(bounds if bounds is not None else backend.grid_bounds, dtype=np.float64).reshape(2, 3)
+    if _exact(backend, exact) and not getattr(backend, "exact_udf", False):
+        return ScalarGrid(box, backend.exact_distance(grid_points(box, resolution)).reshape((resolution,) * 3))
     out = torch.empty(resolution ** 3, dtype=torch.float64, device=backend.torch_device)
     b6 = (ctypes.c_double * 6)(*box.reshape(-1))
     _lib.check(_lib.lib().ddf_udf_grid(backend.handle, b6, int(resolution), int(n_dirs), int(bool(polish)),

@@ -203,6 +203,22 @@ def main_mesh():
     cc = render.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4.0, width=21, height=21)
     out["cube_depth"] = render.render_depth(cube, cc).data
     out["cube_normal"] = render.render_normal(cube, cc, render.RenderConfig(mode="normal")).data
+    # exact distance (mesh.closest_distance) and the exact UDF grid (recon.udf_grid)
+    import types
+    if "skimage" not in sys.modules:
+        sk, skm = types.ModuleType("skimage"), types.ModuleType("skimage.measure")
+        skm.marching_cubes = None
+        sk.measure = skm
+        sys.modules["skimage"], sys.modules["skimage.measure"] = sk, skm
+    from ddfield import recon
+    pts = np.random.default_rng(21).uniform(-2.0, 2.0, (3000, 3))
+    pts[:600] *= 0.55                                   # many near / inside the surface
+    bm = meshes.blob(3, 0)
+    out["closest_pts"] = pts
+    out["closest_blob"] = field.OracleField(bm).exact_distance(pts)
+    assert np.array_equal(out["closest_blob"], field.BruteForceField(bm).exact_distance(pts))
+    out["closest_cube"] = field.OracleField(meshes.cube(0.8)).exact_distance(pts)
+    out["udf_grid_blob"] = recon.udf_grid(field.OracleField(bm), resolution=12).values
     path = os.path.join(HERE, "reference_golden_mesh.npz")
     np.savez_compressed(path, **out)
     print("wrote", path, {k: getattr(v, "shape", None) for k, v in out.items()})
