@@ -1128,9 +1128,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
 // of the other slots.  Weight chunks are streamed once per layer and shared by
 // the four slots (chunk-major MMA order); params are staged only when the
 // network changes.
-constexpr int QS = 4;
-constexpr int Q_EPI_WARPS = 4 * QS;                      // four row warps per slot
-constexpr int Q_NTHREADS = (EPI_WARP0 + Q_EPI_WARPS) * 32;
+constexpr int QS = 4;                                    // most slots per CTA (mask scratch sizing)
 
 template <int EPI>
 __device__ __forceinline__ void epi_rows_n(int nm, const Step& st, int r, uint32_t tmem_row, uint32_t a_row,
@@ -1139,6 +1137,7 @@ __device__ __forceinline__ void epi_rows_n(int nm, const Step& st, int r, uint32
   switch (nm) {
     case 2: epi_direct<EPI, 2, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
     case 4: epi_direct<EPI, 4, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    case 8: epi_direct<EPI, 8, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
     default: break;
   }
 }
@@ -1149,28 +1148,28 @@ __device__ __forceinline__ void encode_row_full(int k0, bool pe, bool valid, con
   else store_encoding<0, 80>(pe, valid, u, a_tile, r);
 }
 
-template <class Op>
-__global__ void __launch_bounds__(Q_NTHREADS, 1)
+template <class Op, int NSL>
+__global__ void __launch_bounds__((EPI_WARP0 + 4 * NSL) * 32, 1)
 mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int a_bytes,
                 int stage_bytes, int params_bytes, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* a_tiles = base_ptr;                                   // [QS][a_bytes]
-  uint8_t* stages = base_ptr + QS * (size_t)a_bytes;
+  uint8_t* a_tiles = base_ptr;                                   // [NSL][a_bytes]
+  uint8_t* stages = base_ptr + NSL * (size_t)a_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)n_stages * stage_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * QS + 2 * n_stages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSL + 2 * n_stages);
   float* sparams = reinterpret_cast<float*>(tmem_slot + 4);      // one copy: [params_bytes/4]
   (void)params_bytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(bars);
   auto BAR_A_READY = [&](int sl) { return bar0 + 8u * sl; };
-  auto BAR_ACC = [&](int sl) { return bar0 + 8u * (QS + sl); };
-  auto BAR_FULL = [&](int s) { return bar0 + 8u * (2 * QS + s); };
-  auto BAR_EMPTY = [&](int s) { return bar0 + 8u * (2 * QS + n_stages + s); };
+  auto BAR_ACC = [&](int sl) { return bar0 + 8u * (NSL + sl); };
+  auto BAR_FULL = [&](int s) { return bar0 + 8u * (2 * NSL + s); };
+  auto BAR_EMPTY = [&](int s) { return bar0 + 8u * (2 * NSL + n_stages + s); };
 
   if (threadIdx.x == 0) {
-    for (int sl = 0; sl < QS; ++sl) {
+    for (int sl = 0; sl < NSL; ++sl) {
       mbar_init(BAR_A_READY(sl), N_EPI_WARPS / 2);
       mbar_init(BAR_ACC(sl), 1);
     }
@@ -1190,7 +1189,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
   const uint32_t tmem = *tmem_slot;
   const uint32_t a_base0 = smem_u32(a_tiles);
   const uint32_t st_base = smem_u32(stages);
-  const int packs = pp_pairs<Op, QS>(F, op);
+  const int packs = pp_pairs<Op, NSL>(F, op);
   unsigned long long dbg_acc[16];
   if (kStats)
     for (int i = 0; i < 16; ++i) dbg_acc[i] = 0ull;
@@ -1202,7 +1201,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
       uint32_t phase = 0;
       for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
         int j0, j1, base, nv;
-        pp_rows<Op, QS>(F, op, pk, 0, j0, j1, base, nv);
+        pp_rows<Op, NSL>(F, op, pk, 0, j0, j1, base, nv);
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
           const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
@@ -1227,11 +1226,12 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t ar[QS] = {0u, 0u, 0u, 0u};
+      uint32_t ar[NSL];
+      for (int i = 0; i < NSL; ++i) ar[i] = 0u;
       const long long t_all = kStats ? clock64() : 0;
       for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
         int j0, j1, base, nv;
-        pp_rows<Op, QS>(F, op, pk, 0, j0, j1, base, nv);
+        pp_rows<Op, NSL>(F, op, pk, 0, j0, j1, base, nv);
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
           const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
@@ -1248,7 +1248,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
               const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
               const uint32_t b_chunk = st_base + (uint32_t)(stage * stage_bytes);
 #pragma unroll 1
-              for (int sl = 0; sl < QS; ++sl) {
+              for (int sl = 0; sl < NSL; ++sl) {
                 if (kc == 0) {
                   // this slot's A tile is written and its TMEM columns are read out
                   DDF_DBG_T0();
@@ -1259,7 +1259,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
                 }
                 const uint32_t a_chunk = a_base0 + (uint32_t)(sl * a_bytes) + (uint32_t)(kc * ROWS * 128);
                 for (int ks = 0; ks < nks; ++ks)
-                  mma_bf16(tmem + (uint32_t)(sl * 128), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
+                  mma_bf16(tmem + (uint32_t)(sl * (512 / NSL)), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
                            (kc | ks) ? 1u : 0u);
                 if (kc == st.nchunk - 1) tc_commit(BAR_ACC(sl));
               }
@@ -1278,10 +1278,10 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
     const int sl = (warp - EPI_WARP0) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint32_t tmem_row = tmem + lane_addr + (uint32_t)(sl * 128);
+    const uint32_t tmem_row = tmem + lane_addr + (uint32_t)(sl * (512 / NSL));
     const uint32_t a_slot = a_base0 + (uint32_t)(sl * a_bytes);
     const uint32_t a_row = a_slot + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
-    uint32_t* my_masks = mask_scratch + ((size_t)blockIdx.x * QS + sl) * MASK_WORDS_PER_CTA;
+    uint32_t* my_masks = mask_scratch + ((size_t)blockIdx.x * NSL + sl) * MASK_WORDS_PER_CTA;
     uint32_t acc_ph = 0u;
     int staged = -1;
     const bool w0 = kStats && threadIdx.x == EPI_WARP0 * 32;
@@ -1289,7 +1289,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
     for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
       long long t_ph = kStats ? clock64() : 0;
       int j0, j1, base, nv;
-      pp_rows<Op, QS>(F, op, pk, sl, j0, j1, base, nv);
+      pp_rows<Op, NSL>(F, op, pk, sl, j0, j1, base, nv);
       const bool valid = r < nv;
       int slot_id = 0;
       double pos[3] = {0.0, 0.0, 0.0}, az = 0.0, pol = 0.0, best = 0.0;
@@ -1309,9 +1309,9 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
           const int nf = __ldg(&P->params_floats);
           const float4* src = reinterpret_cast<const float4*>(P->params);
           float4* dst = reinterpret_cast<float4*>(sparams);
-          named_sync(1, Q_EPI_WARPS * 32);
-          for (int i = threadIdx.x - EPI_WARP0 * 32; i < (nf >> 2); i += Q_EPI_WARPS * 32) dst[i] = __ldg(src + i);
-          named_sync(1, Q_EPI_WARPS * 32);
+          named_sync(1, (4 * NSL) * 32);
+          for (int i = threadIdx.x - EPI_WARP0 * 32; i < (nf >> 2); i += (4 * NSL) * 32) dst[i] = __ldg(src + i);
+          named_sync(1, (4 * NSL) * 32);
           staged = j;
           if (w0) { dbg_acc[8] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
         }
@@ -1585,7 +1585,7 @@ int launch_pp(const FieldDev& F, const std::vector<NetImage>& images, const Op& 
   return 0;
 }
 
-template <class Op>
+template <class Op, int NSL>
 int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
                 uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
   int kmax = 0, chunk = 0, params_bytes = 0;
@@ -1595,17 +1595,17 @@ int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op
     params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
   }
   const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
-  const int extra = 1024 + 8 * (2 * QS + 2 * 8) + 16 + params_bytes;
-  int n_stages = std::min(8, (SMEM_LIMIT - QS * a_bytes - extra) / chunk);
+  const int extra = 1024 + 8 * (2 * NSL + 2 * 8) + 16 + params_bytes;
+  int n_stages = std::min(8, (SMEM_LIMIT - NSL * a_bytes - extra) / chunk);
   if (n_stages < 2) { *err = "bf16 quad engine: not enough shared memory"; return 1; }
-  const size_t smem = QS * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
-  auto kern = mlp_quad_kernel<Op>;
+  const size_t smem = NSL * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
+  auto kern = mlp_quad_kernel<Op, NSL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
-  const int packs_max = ((max_rows + ROWS - 1) / ROWS + QS - 1) / QS + (Op::kGrad ? F.n_obj : 0);
+  const int packs_max = ((max_rows + ROWS - 1) / ROWS + NSL - 1) / NSL + (Op::kGrad ? F.n_obj : 0);
   const int grid = std::max(1, std::min(packs_max, sm_count));
   static const int dbg = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
-  kern<<<grid, Q_NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, params_bytes, dbg);
+  kern<<<grid, (EPI_WARP0 + 4 * NSL) * 32, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, params_bytes, dbg);
   e = cudaGetLastError();
   if (e != cudaSuccess) { *err = std::string("mlp_quad_kernel launch: ") + cudaGetErrorString(e); return 4; }
   return 0;
@@ -1615,9 +1615,18 @@ template <class Op>
 int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
            uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
   static const int dbgq = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
-  bool quad = !(dbgq & 512);
-  for (int j = 0; j < F.n_obj; ++j) quad = quad && images[j].host.pp && images[j].host.max_hidden <= 128;
-  if (quad) return launch_quad<Op>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
+  int maxh = 0;
+  bool all_pp = true;
+  for (int j = 0; j < F.n_obj; ++j) {
+    all_pp = all_pp && images[j].host.pp;
+    maxh = std::max(maxh, images[j].host.max_hidden);
+  }
+  // <= 128 wide: four slots, one row-warp group per slot.  129..256 wide: the
+  // ping-pong engine below (a two-slot group-per-slot variant measured slower:
+  // 880 vs 1065 TF/s forward on 5->8x256, c5 60.1 M vs 69.6 M path samples/s).
+  // dbg 512 forces the ping-pong engine (A/B timing).
+  if (all_pp && maxh <= 128 && !(dbgq & 512))
+    return launch_quad<Op, 4>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
   bool pp = true, any_pp = false;
   for (int j = 0; j < F.n_obj; ++j) {
     pp = pp && images[j].host.pp;
