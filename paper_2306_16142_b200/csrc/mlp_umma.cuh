@@ -340,6 +340,31 @@ __device__ __forceinline__ void pe_tables(const double u[5], float (&sn)[DDF_PE_
     }
   }
 }
+// Chain rule through the 65-D encoding for the tensor-core engines: the same
+// fp32 sin/cos tables as the forward encoding (one sincospif per input and
+// the double-angle recurrence), fp32 accumulation.  The gradient entering
+// here is already fp32 from TMEM; the f64 restatement (field_kernels.cuh
+// pe_chain) is kept for the fp32 SIMT parity engine.
+template <class G>
+__device__ __forceinline__ void pe_chain_tc(bool pe, const double u[5], G g, double out[5]) {
+  float acc[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) acc[j] = g(j);
+  if (pe) {
+    float sn[DDF_PE_OCTAVES][5], cs[DDF_PE_OCTAVES][5];
+    pe_tables(u, sn, cs);
+#pragma unroll
+    for (int o = 0; o < DDF_PE_OCTAVES; ++o) {
+      const float f = (float)(1 << o) * 3.14159265358979f;
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        acc[j] = fmaf(f * cs[o][j], g(5 + 10 * o + j), fmaf(-f * sn[o][j], g(5 + 10 * o + 5 + j), acc[j]));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 5; ++j) out[j] = (double)acc[j];
+}
+
 template <int LO, int HI>
 __device__ __forceinline__ void store_encoding(bool pe, bool valid, const double u[5], uint32_t a_tile, int r) {
   float sn[DDF_PE_OCTAVES][5], cs[DDF_PE_OCTAVES][5];
@@ -673,7 +698,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                       op.store_grad_raw(slot, [&](int k) { return (double)g[k]; });
                     } else {
                       double g5[5];
-                      pe_chain(net, u, [&](int k) { return (double)g[k]; }, g5);
+                      pe_chain_tc(net.encoding == ENC_PE6, u, [&](int k) { return g[k]; }, g5);
                       op.store_grad(slot, g5);
                     }
                   }
@@ -1067,7 +1092,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
                       op.store_grad_raw(slot_id[sl], [&](int k) { return (double)g[k]; });
                     } else {
                       double g5[5];
-                      pe_chain(net, u[sl], [&](int k) { return (double)g[k]; }, g5);
+                      pe_chain_tc(net.encoding == ENC_PE6, u[sl], [&](int k) { return g[k]; }, g5);
                       op.store_grad(slot_id[sl], g5);
                     }
                   }
@@ -1358,7 +1383,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
                   op.store_grad_raw(slot_id, [&](int kk) { return (double)gr[kk]; });
                 } else {
                   double g5[5];
-                  pe_chain(net, u, [&](int kk) { return (double)gr[kk]; }, g5);
+                  pe_chain_tc(net.encoding == ENC_PE6, u, [&](int kk) { return gr[kk]; }, g5);
                   op.store_grad(slot_id, g5);
                 }
               }
