@@ -48,9 +48,9 @@ __device__ __forceinline__ void stage_weights(const float* __restrict__ Wkn, int
 // out[n][m] = epi( sum_k in[k][m] * Wkn[k][n] (+ bias[n]) )
 // Wkn: [K][N] row-major in global memory (K, N multiples of 16).
 // Register tile 8 rows x RN columns per thread: tx = tid % TXM owns rows
-// [8 tx, 8 tx + 8), ty = tid / TXM owns columns {4 ty + j} (+ 128 for the
-// second four when RN = 8) of each 256-column chunk -- 64 FFMA per four
-// 16-byte shared loads at M = 64.  Weight chunks are double-buffered with
+// {4 tx + i} and {M/2 + 4 tx + i} (i < 4), ty = tid / TXM owns columns
+// {4 ty + j} (+ NCT/2 for the second four when RN = 8) of each chunk -- 64
+// FFMA per four 16-byte shared loads at M = 64.  Weight chunks are double-buffered with
 // cp.async and each k step's operands are loaded one step ahead.
 template <int M, int NCT>
 __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const float* __restrict__ bias,
@@ -59,7 +59,9 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
   constexpr int RM = 8, TXM = M / RM, TYN = NT / TXM, RN = NCT / TYN;
   static_assert(RN == 4 || RN == 8, "register tile");
   const int tid = threadIdx.x, tx = tid % TXM, ty = tid / TXM;
-  const int m0 = tx * RM;
+  // rows {4 tx + i} and {M/2 + 4 tx + i}, i < 4: a warp's 16-byte loads and
+  // stores of one half cover 128 contiguous bytes (no bank conflicts)
+  const int m0 = tx * 4, mh = M / 2;
   const int nk = (K + KC - 1) / KC;
   auto col = [&](int j) { return RN == 8 ? (j < 4 ? ty * 4 + j : NCT / 2 + ty * 4 + (j - 4)) : ty * 4 + j; };
   for (int n0 = 0; n0 < N; n0 += NCT) {
@@ -81,7 +83,7 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
       __syncthreads();
       const float* wsc = ws + (c & 1) * KC * NCT + ty * 4;
       const float* ai = act_in + (size_t)k0 * M + m0;
-      float4 a0 = *reinterpret_cast<const float4*>(ai), a1 = *reinterpret_cast<const float4*>(ai + 4);
+      float4 a0 = *reinterpret_cast<const float4*>(ai), a1 = *reinterpret_cast<const float4*>(ai + mh);
       float4 w0 = *reinterpret_cast<const float4*>(wsc), w1 = w0;
       if constexpr (RN == 8) w1 = *reinterpret_cast<const float4*>(wsc + NCT / 2);
 #pragma unroll 4
@@ -90,7 +92,7 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
         const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
         if (k + 1 < kc) {   // operands of step k + 1 in flight while step k computes
           a0 = *reinterpret_cast<const float4*>(ai + (k + 1) * M);
-          a1 = *reinterpret_cast<const float4*>(ai + (k + 1) * M + 4);
+          a1 = *reinterpret_cast<const float4*>(ai + (k + 1) * M + mh);
           w0 = *reinterpret_cast<const float4*>(wsc + (k + 1) * NCT);
           if constexpr (RN == 8) w1 = *reinterpret_cast<const float4*>(wsc + (k + 1) * NCT + NCT / 2);
         }
@@ -101,7 +103,7 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
       }
       __syncthreads();   // this buffer is refilled two chunks later
     }
-    // epilogue: a thread's 8 rows of one column are contiguous -> two vector stores
+    // epilogue: each half of a thread's rows of one column -> one vector store
 #pragma unroll
     for (int j = 0; j < RN; ++j) {
       const int cc = col(j);
@@ -109,8 +111,13 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
       const int n = n0 + (live ? cc : 0);
       const float bn = (live && bias != nullptr) ? __ldg(bias + n) : 0.f;
       float v[RM];
-      uint32_t bits = 0;
-      const uint32_t mw = (mode == EPI_MASKMUL && live) ? mask_in[n * (M / 32) + (m0 >> 5)] >> (m0 & 31) : 0u;
+      uint32_t bits = 0;   // bit i: row (i < 4 ? m0 + i : mh + m0 + i - 4)
+      uint32_t mw = 0u;
+      if (mode == EPI_MASKMUL && live) {
+        const uint32_t* mk = mask_in + n * (M / 32);
+        const uint32_t lo = mk[m0 >> 5] >> (m0 & 31), hi = mk[(mh + m0) >> 5] >> ((mh + m0) & 31);
+        mw = (lo & 15u) | ((hi & 15u) << 4);
+      }
 #pragma unroll
       for (int i = 0; i < RM; ++i) {
         float x = acc[i][j];
@@ -126,14 +133,25 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
       }
       if (live) {
         *reinterpret_cast<float4*>(act_out + n * M + m0) = make_float4(v[0], v[1], v[2], v[3]);
-        *reinterpret_cast<float4*>(act_out + n * M + m0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        *reinterpret_cast<float4*>(act_out + n * M + mh + m0) = make_float4(v[4], v[5], v[6], v[7]);
       }
       if (mode == EPI_RELU_MASK) {
-        // OR the four lanes that share one 32-row mask word (aligned lane groups)
-        uint32_t word = bits << (m0 & 31);
-        word |= __shfl_xor_sync(0xffffffffu, word, 1);
-        word |= __shfl_xor_sync(0xffffffffu, word, 2);
-        if (live && (tx & 3) == 0) mask_out[n * (M / 32) + (m0 >> 5)] = word;
+        // mask words: rows [0, 32) ... of each half, OR-ed over the TXM lanes of one row group
+        uint32_t lo = (bits & 15u) << (m0 & 31), hi = ((bits >> 4) & 15u) << ((mh + m0) & 31);
+#pragma unroll
+        for (int o = 1; o < TXM; o <<= 1) {
+          lo |= __shfl_xor_sync(0xffffffffu, lo, o);
+          hi |= __shfl_xor_sync(0xffffffffu, hi, o);
+        }
+        if (live && tx == 0) {
+          uint32_t* mk = mask_out + n * (M / 32);
+          if constexpr (M == 64) {
+            mk[0] = lo;
+            mk[1] = hi;
+          } else {
+            mk[0] = lo | hi;
+          }
+        }
       }
     }
   }
