@@ -93,7 +93,7 @@ struct Prof {
 struct ddf_field_s {
   Prof prof;
   FieldDev F{};                 // host copy holding device pointers
-  FieldDev* F_dev = nullptr;    // device copy (BounceOp reads albedos through it)
+  FieldDev* F_dev = nullptr;    // device copy (bounce_kernel reads albedos through it)
   std::vector<void*> weights;   // device weight allocations
   std::vector<umma::NetImage> images;
   int device = 0;

@@ -9,7 +9,7 @@
 //   QueryOp       NeuralField.query_batch     field.py:248-258
 //   TraceStepOp   one step of trace_batch     field.py:274-288
 //   NormalOp      NeuralField.normal_batch    field.py:295-317
-// (BounceOp, the fused normal+shade+sample stage of render_path, lives in
+// (GradOutOp, the gradient pass of render_path's bounce stage, lives in
 // wavefront.cuh.)
 #pragma once
 #include "ddf_common.cuh"
