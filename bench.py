@@ -606,6 +606,38 @@ def main():
                              "launches": stp["gradient_launches"],
                              "tflops": grad_flops / (stp["ms_gradient"] / 1e3) / 1e12 if stp["ms_gradient"] else None},
                 "compaction_ms": stp["ms_compact"], "other_ms": stp["ms_other"], "profiled_step_ms": stp["ms_total"]}
+    # wavefront compaction against HBM: per compaction call the
+    # flags are read twice (plus 4 B object ids twice when bucketed) and 4 B
+    # are written per survivor; the survivors are exactly the MLP rows
+    import math
+    lo_b, hi_b = np.asarray(C.SCENE_BOX if w.get("scene") else C.UNIT_BOX)
+    diag = float(np.sqrt(((hi_b - lo_b) ** 2).sum()))
+    max_steps = math.ceil(diag / (0.9 * C.delta(name))) + 4
+    samples = int(stp["path_samples"])
+    calls = max_steps * (1 + cfg.bounces) + cfg.bounces
+    cbytes = 2 * samples * calls + (8 * samples * cfg.bounces if w.get("scene") else 0) \
+        + 4 * (stp["forward_rows"] + stp["gradient_rows"])
+    hbm = float(peaks.get("hbm_gbs", 6540.5))
+    if stp["ms_compact"]:
+        gbps = cbytes / (stp["ms_compact"] / 1e3) / 1e9
+        roofline["compaction"] = {"bound": "hbm", "ms": stp["ms_compact"], "bytes": cbytes, "achieved": gbps,
+                                  "peak": hbm, "unit": "GB/s", "frac": gbps / hbm,
+                                  "calls_per_wave": calls, "note": "launch-latency bound below ~8 M slots per call"}
+    # DRAM traffic per launch of the dominant kernel from the committed ncu
+    # --set full capture of this workload (profiles/), next to the
+    # algorithmic path-state bytes of that launch
+    ncu_path = os.path.join(ROOT, "profiles", f"r1_{name}_ncu_v7.json")
+    if os.path.exists(ncu_path):
+        try:
+            g = json.load(open(ncu_path))["gradient_launch"]
+            roofline["traffic"] = g["traffic_bytes"]
+            roofline["traffic_source"] = ("ncu --set full, one %s launch of %.1f ms (%s): %.0f MB DRAM vs ~%.0f MB "
+                                          "algorithmic path state; tensor pipe active %.1f%%" % (
+                                              "mlp_kernel<GradOutOp>", g["duration_ms"], os.path.basename(ncu_path),
+                                              g["traffic_bytes"] / 1e6, g["algorithmic_state_bytes_est"] / 1e6,
+                                              g["tensor_pipe_active_pct_elapsed"]))
+        except Exception:
+            pass
 
     # end to end through the public API: host film out, RNG tables in
     e2e = None
