@@ -208,6 +208,32 @@ def bench_queries(args, rank, world, local):
            "e2e": {"value": n / float(np.mean(te)), "unit": "queries/s", "h2d_bytes_per_step": 2 * n * 24,
                    "d2h_bytes_per_step": n * (8 + 8 + 1 + 4)},
            "gpu_launches": args.steps, "clocks": clk.summary()}
+    # 65,536 rays are launch-latency bound; the large-N sweep
+    # shows the engines' throughput (both precisions, same rays tiled)
+    sweep = []
+    for prc in ("fp32", "bf16"):
+        fs = f if prc == prec else C.build_field("c1", precision=prc)
+        for big in (1 << 20, 1 << 22, 1 << 24):
+            reps = -(-big // n)
+            ob, db = od.repeat(reps, 1)[:big].contiguous(), dd.repeat(reps, 1)[:big].contiguous()
+            tb = torch.empty(big, dtype=torch.float64, device="cuda")
+            hb = torch.empty(big, dtype=torch.uint8, device="cuda")
+            call = lambda: _lib.check(L.ddf_query(fs.handle, P(ob), P(db), big, P(tb), P(hb), None, None,  # noqa: E731
+                                                  ctypes.c_void_p(st.cuda_stream)))
+            call()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(3):
+                call()
+            e1.record(st)
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 3
+            sweep.append({"precision": prc, "rows": big, "ms": t, "queries_per_s": big / (t / 1e3),
+                          "tflops": F * big / (t / 1e3) / 1e12})
+    out["sweep"] = sweep
+    out["sweep_note"] = ("5->4x128->1: 128-wide layers cap UMMA at N = 128, about half the bf16 tensor peak "
+                         "(DESIGN.md section 3); fp32 runs on the FFMA pipe (74 TF/s peak)")
     if rank == 0:
         print(json.dumps(out))
 
