@@ -42,6 +42,13 @@ constexpr int ROWS = 128;
 #define DDF_PIPE_STATS 0
 #endif
 constexpr bool kStats = DDF_PIPE_STATS != 0;
+// DDF_DEBUG_UMMA bits that skip work (timing experiments, wrong results):
+// honoured only in the diagnostics build (-DDDF_PIPE_STATS=1, scratch/).
+constexpr int kUnsafeDbg = 1 | 8 | 128 | 1024;
+inline int debug_bits() {
+  static const int raw = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
+  return kStats ? raw : (raw & ~kUnsafeDbg);
+}
 __device__ unsigned long long g_dbg[16];
 #define DDF_DBG_T0() long long _t0 = kStats ? clock64() : 0
 #define DDF_DBG_ADD(i) do { if (kStats) dbg_acc[i] += (unsigned long long)(clock64() - _t0); } while (0)
@@ -1629,7 +1636,7 @@ int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op
   if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
   const int packs_max = ((max_rows + ROWS - 1) / ROWS + NSL - 1) / NSL + (Op::kGrad ? F.n_obj : 0);
   const int grid = std::max(1, std::min(packs_max, sm_count));
-  static const int dbg = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
+  const int dbg = debug_bits();
   kern<<<grid, (EPI_WARP0 + 4 * NSL) * 32, smem, st>>>(F, op, mask_scratch, n_stages, a_bytes, chunk, params_bytes, dbg);
   e = cudaGetLastError();
   if (e != cudaSuccess) { *err = std::string("mlp_quad_kernel launch: ") + cudaGetErrorString(e); return 4; }
@@ -1639,7 +1646,7 @@ int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op
 template <class Op>
 int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
            uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
-  static const int dbgq = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
+  const int dbgq = debug_bits();
   int maxh = 0;
   bool all_pp = true;
   for (int j = 0; j < F.n_obj; ++j) {
@@ -1670,7 +1677,7 @@ int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op,
   int n_stages = (SMEM_LIMIT - a_bytes - extra) / chunk;
   n_stages = std::min(n_stages, 8);
   if (n_stages < 2) { *err = "bf16 engine: not enough shared memory for the weight pipeline"; return 1; }
-  static const int dbg = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
+  const int dbg = debug_bits();
   if (dbg & 8) n_stages = 8;
   if (dbg & 256) n_stages = std::min(n_stages, 2);
   const size_t smem = (size_t)a_bytes + (size_t)((dbg & 8) ? 1 : n_stages) * chunk + extra;
