@@ -86,11 +86,10 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
       float4 a0 = *reinterpret_cast<const float4*>(ai), a1 = *reinterpret_cast<const float4*>(ai + mh);
       float4 w0 = *reinterpret_cast<const float4*>(wsc), w1 = w0;
       if constexpr (RN == 8) w1 = *reinterpret_cast<const float4*>(wsc + NCT / 2);
-#pragma unroll 4
-      for (int k = 0; k < kc; ++k) {
+      auto kstep = [&](int k, bool more) {
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        if (k + 1 < kc) {   // operands of step k + 1 in flight while step k computes
+        if (more) {   // operands of step k + 1 in flight while step k computes
           a0 = *reinterpret_cast<const float4*>(ai + (k + 1) * M);
           a1 = *reinterpret_cast<const float4*>(ai + (k + 1) * M + mh);
           w0 = *reinterpret_cast<const float4*>(wsc + (k + 1) * NCT);
@@ -100,6 +99,13 @@ __device__ __forceinline__ void gemm_chunks(const float* __restrict__ Wkn, const
         for (int i = 0; i < RM; ++i)
 #pragma unroll
           for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+      };
+      if (kc == KC) {   // full chunk: unrolled, no per-step predicates
+#pragma unroll
+        for (int k = 0; k < KC; ++k) kstep(k, k + 1 < KC);
+      } else {
+#pragma unroll 4
+        for (int k = 0; k < kc; ++k) kstep(k, k + 1 < kc);
       }
       __syncthreads();   // this buffer is refilled two chunks later
     }
