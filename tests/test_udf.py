@@ -177,3 +177,22 @@ def test_gpu_udf_bf16(cuda, ug):
     got = U.udf_many(f1, ug["u_points"][:100], n_dirs=32)
     ref = ug["u_cfg1_many32"]
     assert np.all(np.isfinite(got)) and np.max(np.abs(got - ref)) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_gpu_udf_composite_scene(cuda):
+    """udf_many over an 8-object min-composite field (config-5 layout,
+    EXTENSION): the query row op composes the objects exactly as render does."""
+    from paper_2306_16142_b200 import configs as C
+    from paper_2306_16142_b200 import udf as U
+    from paper_2306_16142_b200.field import CudaNeuralField
+    from paper_2306_16142_b200.neural import kaiming_uniform
+    centers, scale, albedos = C.scene_layout()
+    ms = [kaiming_uniform((5, 32, 32, 1), s) for s in range(10, 18)]
+    f = CudaNeuralField.scene(ms, centers, scale, albedos, DELTA_CFG, bounds=C.SCENE_BOX)
+    of = O.Field([O.Net(m.widths, m.v, m.g, m.b) for m in ms], DELTA_CFG, bounds=C.SCENE_BOX, centers=centers,
+                 scale=scale, albedos=albedos)
+    pts = np.random.default_rng(8).uniform(-1.2, 1.2, (60, 3))
+    raw, ref_raw = U.udf_many(f, pts, n_dirs=48, polish=False), O.udf_many(of, pts, 48, polish=False)
+    assert np.max(np.abs(raw - ref_raw)) <= 1e-5
+    _close_polished(U.udf_many(f, pts, n_dirs=48), O.udf_many(of, pts, 48))
