@@ -70,6 +70,16 @@ typedef struct {
 } ddf_path_config_t;
 
 typedef struct {
+  /* render.RenderConfig fields used by render_depth / render_normal /
+     render_shaded (render.py:106-124, 144-184) */
+  int32_t mode;            /* 0 depth, 1 normal, 2 shaded                   */
+  int32_t ambient;         /* shaded: flat albedo * env_radiance            */
+  double background[3];
+  double light_dir[3];     /* used as given (render.py:181)                 */
+  double albedo, env_radiance;
+} ddf_mode_config_t;
+
+typedef struct {
   uint64_t forward_rows;   /* MLP forward rows evaluated (DDF queries)       */
   uint64_t gradient_rows;  /* MLP input-gradient rows (normals)             */
   uint64_t degenerate;     /* normals that fell back to -d (render.py:133)  */
@@ -155,6 +165,13 @@ int ddf_udf(ddf_field_t f, const double* points, int64_t n, int32_t n_dirs, int3
    order, recon.py:53-58); out (resolution^3,) f64 device.  resolution >= 8. */
 int ddf_udf_grid(ddf_field_t f, const double bbox[6], int32_t resolution, int32_t n_dirs, int32_t polish,
                  double* out, void* stream);
+
+/* render.render_depth / render_normal / render_shaded (render.py:144-184)
+   entirely on the device: pixel-centre rays (render.py:54-75), trace, the
+   normals of the hit pixels (_hit_normals, render.py:127-141) and the shading.
+   out: depth (H*W) f64, +inf on a miss; normal / shaded (H*W*3) f64 RGB, row
+   major.  DDF_ENUMERIC on the normal sign rule. */
+int ddf_render_mode(ddf_field_t f, const ddf_camera_t* cam, const ddf_mode_config_t* cfg, double* out, void* stream);
 
 /* np.random.default_rng(...).random() draw k of a PCG64 stream given its
    (state, inc) (render.py:209,213,222): out[j] = draw idx[j] (device arrays). */

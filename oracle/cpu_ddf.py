@@ -604,7 +604,7 @@ def film_rgb(value, cam: Cam):
 # --------------------------------------------------------------------------
 
 def render_mode(fld: Field, cam: Cam, mode: str, background=(0.0, 0.0, 0.0),
-                light_dir=(1.0, 1.0, 1.0), albedo=0.7, env=1.0, ambient=False):
+                light_dir=tuple(np.array([1.0, 1.0, 1.0]) / np.sqrt(3.0)), albedo=0.7, env=1.0, ambient=False):
     """render.py:144-184: "depth" -> (H, W) t (inf on miss); "normal" /
     "shaded" -> (H, W, 3).  Pixel-centre rays (render.py:62-63)."""
     n = cam.width * cam.height
@@ -622,8 +622,7 @@ def render_mode(fld: Field, cam: Cam, mode: str, background=(0.0, 0.0, 0.0),
     elif ambient:
         rgb[hit] = albedo * env
     else:
-        l = np.asarray(light_dir, dtype=np.float64)
-        l = l / np.linalg.norm(l)
+        l = np.asarray(light_dir, dtype=np.float64)           # used as given (render.py:181)
         rgb[hit] = (albedo * np.maximum(nrm[hit] @ l, 0.0))[:, None]
     return rgb.reshape(cam.height, cam.width, 3)
 

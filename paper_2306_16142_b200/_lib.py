@@ -29,7 +29,7 @@ ENC_RAW5, ENC_PE6 = 0, 1
 
 EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "ddf_field_set_precision",
            "ddf_last_error", "ddf_mlp_forward", "ddf_mlp_input_grad", "ddf_query", "ddf_trace",
-           "ddf_normal", "ddf_render_path", "ddf_mesh_create", "ddf_mesh_intersect", "ddf_mesh_closest", "ddf_udf", "ddf_udf_grid", "ddf_rng_doubles", "ddf_compact",
+           "ddf_normal", "ddf_render_path", "ddf_render_mode", "ddf_mesh_create", "ddf_mesh_intersect", "ddf_mesh_closest", "ddf_udf", "ddf_udf_grid", "ddf_rng_doubles", "ddf_compact",
            "ddf_debug_counters")
 
 
@@ -70,6 +70,11 @@ class PathConfig_t(ctypes.Structure):
                 ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32)]
 
 
+class ModeConfig_t(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("ambient", ctypes.c_int32), ("background", ctypes.c_double * 3),
+                ("light_dir", ctypes.c_double * 3), ("albedo", ctypes.c_double), ("env_radiance", ctypes.c_double)]
+
+
 class RenderStats_t(ctypes.Structure):
     _fields_ = [("forward_rows", ctypes.c_uint64), ("gradient_rows", ctypes.c_uint64),
                 ("degenerate", ctypes.c_uint64), ("path_samples", ctypes.c_uint64),
@@ -108,6 +113,7 @@ def lib():
     L.ddf_rng_doubles.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64), dp, i64, dp, vp]
     L.ddf_compact.argtypes = [dp, i64, dp, dp, vp]
     L.ddf_udf.argtypes = [vp, dp, i64, i32, i32, dp, vp]
+    L.ddf_render_mode.argtypes = [vp, ctypes.POINTER(Camera_t), ctypes.POINTER(ModeConfig_t), dp, vp]
     L.ddf_mesh_create.argtypes = [vp, i64, vp, i64, i32, ctypes.POINTER(vp)]
     L.ddf_mesh_closest.argtypes = [vp, dp, i64, dp, vp]
     L.ddf_mesh_intersect.argtypes = [vp, dp, dp, i64, ctypes.c_double, ctypes.c_double, dp, dp, dp, dp, vp]

@@ -912,6 +912,85 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   return DDF_OK;
 }
 
+int ddf_render_mode(ddf_field_t f, const ddf_camera_t* cam, const ddf_mode_config_t* cfg, double* out, void* stream) {
+  if (!has_geometry(f)) return fail(DDF_EUSAGE, "field has no network");
+  if (!cam || !cfg || !out) return fail(DDF_EUSAGE, "null argument");
+  if (cfg->mode < 0 || cfg->mode > 2) return fail(DDF_EUSAGE, "unknown render mode");
+  if (cam->width < 1 || cam->height < 1) return fail(DDF_EUSAGE, "film dimensions must be >= 1");
+  const int64_t P64 = (int64_t)cam->width * cam->height;
+  if (P64 > (1ll << 30)) return fail(DDF_EUSAGE, "film too large");
+  const int P = (int)P64;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(f->device));
+  if (int rc = ensure_small(f)) return rc;
+  Small sm = small_of(f);
+  f->prof.reset(false);
+  CUDA_TRY(cudaMemsetAsync(f->small.p, 0, 4096, st));
+  CUDA_TRY(f->st_o.ensure(sizeof(double) * 3 * P));
+  CUDA_TRY(f->st_d.ensure(sizeof(double) * 3 * P));
+  CUDA_TRY(f->st_tacc.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_texit.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_t.ensure(sizeof(double) * P));
+  CUDA_TRY(f->st_hit.ensure(P));
+  CUDA_TRY(f->st_march.ensure(P));
+  CUDA_TRY(f->st_obj.ensure(sizeof(int) * P));
+  CUDA_TRY(f->st_u34.ensure(sizeof(double) * 2 * P));
+  CUDA_TRY(f->st_g3.ensure(sizeof(double) * 3 * P));
+  CUDA_TRY(f->list.ensure(sizeof(int) * P));
+  CUDA_TRY(f->list2.ensure(sizeof(int) * P));
+  PathState S{};
+  S.o = f->st_o.as<double>(); S.d = f->st_d.as<double>();
+  S.t_acc = f->st_tacc.as<double>(); S.t_exit = f->st_texit.as<double>(); S.t = f->st_t.as<double>();
+  S.hit = f->st_hit.as<uint8_t>(); S.march = f->st_march.as<uint8_t>();
+  S.obj = f->st_obj.as<int>(); S.u34 = f->st_u34.as<double>(); S.g3 = f->st_g3.as<double>();
+  MarchState ms{};
+  ms.o = S.o; ms.d = S.d; ms.t_acc = S.t_acc; ms.t_exit = S.t_exit; ms.alive = S.march;
+  ms.t_out = S.t; ms.hit = S.hit; ms.obj = S.obj; ms.u34 = S.u34;
+  CamDev C{};
+  for (int k = 0; k < 3; ++k) {
+    C.pos[k] = cam->position[k]; C.fwd[k] = cam->forward[k]; C.right[k] = cam->right[k]; C.up[k] = cam->up_ortho[k];
+  }
+  C.tan_half = cam->tan_half; C.aspect = cam->aspect; C.W = cam->width; C.H = cam->height;
+  const int g = (P + 255) / 256;
+  camera_center_kernel<<<g, 256, 0, st>>>(f->F, C, S, P);
+  CUDA_TRY(cudaGetLastError());
+  // trace_batch (render.py:148,158,173)
+  if (f->F.is_mesh) {
+    mesh::trace_paths_kernel<<<g, 256, 0, st>>>(f->M, S, nullptr, nullptr, P);
+    CUDA_TRY(cudaGetLastError());
+  } else if (int rc = march(f, ms, P, f->list2.as<int>(), sm.stats + 0, st)) {
+    return rc;
+  }
+  if (cfg->mode != 0) {
+    // normals of the hit pixels (render.py:130-131)
+    const int nobj = f->F.n_obj;
+    if (int rc = compact_flags(f, S.hit, nobj > 1 ? S.obj : nullptr, P, std::max(1, nobj), f->list.as<int>(),
+                               sm.seg, sm.count2, sm.stats + 1, st))
+      return rc;
+    if (f->F.is_mesh) {
+      mesh::face_normal_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->M, S, f->list.as<int>(), sm.count2);
+      CUDA_TRY(cudaGetLastError());
+    } else {
+      GradOutOp op{};
+      op.list = f->list.as<int>(); op.count = sm.count2; op.n = P;
+      op.seg = nobj > 1 ? sm.seg : nullptr;
+      op.S = S; op.backoff = f->F.backoff;
+      if (int rc = run_mlp(f, f->F, op, P, true, st)) return rc;
+    }
+  }
+  ModeDev m{};
+  m.mode = cfg->mode; m.ambient = cfg->ambient;
+  for (int k = 0; k < 3; ++k) { m.bg[k] = cfg->background[k]; m.light[k] = cfg->light_dir[k]; }
+  m.albedo = cfg->albedo; m.env = cfg->env_radiance;
+  mode_shade_kernel<<<g, 256, 0, st>>>(m, S, P, out, sm.err, sm.stats + 2);
+  CUDA_TRY(cudaGetLastError());
+  int host_small[32];
+  CUDA_TRY(cudaMemcpyAsync(host_small, f->small.p, sizeof(host_small), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (host_small[18] & DEVERR_SIGN_RULE) return fail(DDF_ENUMERIC, "normal sign rule violated: n . dir >= 0");
+  return DDF_OK;
+}
+
 namespace {
 __global__ void rng_kernel(const PcgStream* st, const uint64_t* idx, int n, double* out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;

@@ -98,6 +98,70 @@ __global__ void camera_kernel(const FieldDev F, const CamDev C, const WaveDev w,
   begin_trace(F, S, p, o, d);
 }
 
+// render.py:54-75 pixel_rays at pixel centres (offsets 0.5) for the
+// single-bounce modes; slot p = pixel p
+__global__ void camera_center_kernel(const FieldDev F, const CamDev C, const PathState S, int P) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const double px = (double)(p % C.W), py = (double)(p / C.W);
+  const double sx = dmul(dmul(dsub(ddiv(dmul(2.0, dadd(px, 0.5)), (double)C.W), 1.0), C.tan_half), C.aspect);
+  const double sy = dmul(dsub(1.0, ddiv(dmul(2.0, dadd(py, 0.5)), (double)C.H)), C.tan_half);
+  d3 d = mk3(dadd(dadd(C.fwd[0], dmul(sx, C.right[0])), dmul(sy, C.up[0])),
+             dadd(dadd(C.fwd[1], dmul(sx, C.right[1])), dmul(sy, C.up[1])),
+             dadd(dadd(C.fwd[2], dmul(sx, C.right[2])), dmul(sy, C.up[2])));
+  const double nr = norm3(d);
+  d = mk3(ddiv(d.x, nr), ddiv(d.y, nr), ddiv(d.z, nr));
+  const d3 o = mk3(C.pos[0], C.pos[1], C.pos[2]);
+  st3(S.o, p, o);
+  st3(S.d, p, d);
+  begin_trace(F, S, p, o, d);
+}
+
+struct ModeDev {
+  int mode, ambient;
+  double bg[3], light[3], albedo, env;
+};
+
+// render.py:144-184 per pixel from the trace (t, hit) and, for hit pixels,
+// the spatial gradient / face cross product in g3 (_hit_normals semantics)
+__global__ void mode_shade_kernel(const ModeDev m, const PathState S, int P, double* out, int* err,
+                                  unsigned long long* degenerate) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const bool h = S.hit[p];
+  if (m.mode == 0) {
+    out[p] = h ? S.t[p] : INFINITY;
+    return;
+  }
+  double rgb[3] = {m.bg[0], m.bg[1], m.bg[2]};
+  if (h) {
+    const d3 d = ld3(S.d, p), g = ld3(S.g3, p);
+    const double nr = norm3(g);
+    d3 n;
+    if (nr >= 1e-12) {
+      n = mk3(ddiv(g.x, nr), ddiv(g.y, nr), ddiv(g.z, nr));
+      if (dot3(n, d) > 0.0) n = mk3(-n.x, -n.y, -n.z);
+    } else {
+      n = mk3(-d.x, -d.y, -d.z);
+      atomicAdd(degenerate, 1ull);
+    }
+    if (!(dot3(n, d) < 0.0)) atomicOr(err, (int)DEVERR_SIGN_RULE);
+    if (m.mode == 1) {
+      rgb[0] = dmul(0.5, dadd(n.x, 1.0));
+      rgb[1] = dmul(0.5, dadd(n.y, 1.0));
+      rgb[2] = dmul(0.5, dadd(n.z, 1.0));
+    } else {
+      const double c = m.ambient ? dmul(m.albedo, m.env)
+                                 : dmul(m.albedo, fmax(dadd(dadd(dmul(n.x, m.light[0]), dmul(n.y, m.light[1])),
+                                                            dmul(n.z, m.light[2])), 0.0));
+      rgb[0] = rgb[1] = rgb[2] = c;
+    }
+  }
+  out[3 * (int64_t)p] = rgb[0];
+  out[3 * (int64_t)p + 1] = rgb[1];
+  out[3 * (int64_t)p + 2] = rgb[2];
+}
+
 // render.py:218-219  escape of primary rays, alive = hit
 __global__ void after_primary_kernel(const WaveDev w, const PathState S, int P) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;

@@ -207,8 +207,40 @@ def _trace_with_obj(backend, o, d):
     return t, hit, None
 
 
+_MODE_IDS = {"depth": 0, "normal": 1, "shaded": 2}
+
+
+def _device_backend(backend) -> bool:
+    return getattr(backend, "handle", None) is not None and hasattr(backend, "torch_device")
+
+
+def render_mode_device(backend, camera, config, mode: str):
+    """render.py:144-184 on the device (ddf_render_mode): pixel-centre rays,
+    trace, hit normals and shading without host round trips.  Returns the
+    (H, W) depth or (H, W, 3) RGB array."""
+    m = _lib.ModeConfig_t()
+    m.mode = _MODE_IDS[mode]
+    m.ambient = int(bool(getattr(config, "ambient", False)))
+    for k in range(3):
+        m.background[k] = float(config.background[k])
+        m.light_dir[k] = float(np.asarray(config.light_dir, dtype=np.float64)[k])
+    m.albedo = float(config.albedo)
+    m.env_radiance = float(config.env_radiance)
+    W, H = camera.width, camera.height
+    out = torch.empty(W * H * (1 if mode == "depth" else 3), dtype=torch.float64, device=backend.torch_device)
+    cam = camera_struct(camera)
+    _lib.check(_lib.lib().ddf_render_mode(backend.handle, ctypes.byref(cam), ctypes.byref(m),
+                                          ctypes.c_void_p(out.data_ptr()),
+                                          ctypes.c_void_p(torch.cuda.current_stream(backend.torch_device).cuda_stream)))
+    a = out.cpu().numpy()
+    return a.reshape(H, W) if mode == "depth" else a.reshape(H, W, 3)
+
+
 def render_depth(backend, camera, config=None):
     """render.py:144-150: field values per pixel, non-finite on a miss."""
+    if _device_backend(backend):
+        return Framebuffer(camera.width, camera.height,
+                           render_mode_device(backend, camera, config or RenderConfig(mode="depth"), "depth"))
     o, d = pixel_rays(camera)
     t, hit, _ = _trace_with_obj(backend, o, d)
     return Framebuffer(camera.width, camera.height, np.where(hit, t, np.inf).reshape(camera.height, camera.width))
@@ -217,6 +249,8 @@ def render_depth(backend, camera, config=None):
 def render_normal(backend, camera, config=None):
     """render.py:153-164: normals mapped (n + 1)/2, misses get the background."""
     config = config or RenderConfig(mode="normal")
+    if _device_backend(backend):
+        return Framebuffer(camera.width, camera.height, render_mode_device(backend, camera, config, "normal"))
     o, d = pixel_rays(camera)
     t, hit, obj = _trace_with_obj(backend, o, d)
     nrm = _hit_normals(backend, o, d, t, hit, obj)
@@ -227,8 +261,11 @@ def render_normal(backend, camera, config=None):
 
 
 def render_shaded(backend, camera, config=None):
-    """render.py:167-184: Lambertian under a directional light (or ambient)."""
+    """render.py:167-184: Lambertian under a directional light (used as
+    given, render.py:181) or the flat ambient term."""
     config = config or RenderConfig(mode="shaded")
+    if _device_backend(backend):
+        return Framebuffer(camera.width, camera.height, render_mode_device(backend, camera, config, "shaded"))
     o, d = pixel_rays(camera)
     t, hit, obj = _trace_with_obj(backend, o, d)
     nrm = _hit_normals(backend, o, d, t, hit, obj)
@@ -237,8 +274,7 @@ def render_shaded(backend, camera, config=None):
     if config.ambient:
         shade = np.full(int(hit.sum()), config.albedo * config.env_radiance)
     else:
-        l = np.asarray(config.light_dir, dtype=np.float64)
-        shade = config.albedo * np.maximum(nrm[hit] @ (l / np.linalg.norm(l)), 0.0)
+        shade = config.albedo * np.maximum(nrm[hit] @ np.asarray(config.light_dir, dtype=np.float64), 0.0)
     rgb[hit] = shade[:, None]
     return Framebuffer(camera.width, camera.height, rgb.reshape(camera.height, camera.width, 3))
 

@@ -51,7 +51,7 @@ def test_struct_layouts_match_header(tmp_path):
         pytest.skip("no gcc")
     src = tmp_path / "sz.c"
     fields = {"ddf_camera_t": _lib.Camera_t, "ddf_path_config_t": _lib.PathConfig_t,
-              "ddf_render_stats_t": _lib.RenderStats_t}
+              "ddf_render_stats_t": _lib.RenderStats_t, "ddf_mode_config_t": _lib.ModeConfig_t}
     body = []
     for cname, py in fields.items():
         body.append(f'printf("%zu\\n", sizeof({cname}));')

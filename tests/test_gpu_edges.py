@@ -171,3 +171,61 @@ def test_config4_network_path_parity_fp32():
           f"pixels differing {np.mean(d > 1e-6):.1%}, RMSE {np.sqrt(np.mean(d ** 2)):.3g}")
     assert abs(img.mean() - ref.mean()) <= 0.01 * ref.mean()
     assert np.mean(d > 1e-6) <= 0.25
+
+
+class _ProtocolOnly:
+    """Hides the device handle so render_* take the host protocol path
+    (pixel_rays on the host, trace_batch / normal_batch calls)."""
+
+    def __init__(self, f):
+        self._f = f
+
+    def trace_batch(self, o, d):
+        return self._f.trace_batch(o, d)
+
+    def trace_with_objects(self, o, d):
+        return self._f.trace_with_objects(o, d)
+
+    def normal_batch(self, o, d, t_hit=None, obj=None):
+        return self._f.normal_batch(o, d, t_hit=t_hit, obj=obj)
+
+
+@pytest.mark.parametrize("scene", [False, True])
+def test_device_render_modes_equal_protocol_path(scene):
+    """ddf_render_mode (everything on the device) == the host protocol path
+    on the same field: depth and normal bit for bit, shading to the last ulp
+    of the light dot product (numpy's matvec may fuse differently)."""
+    from paper_2306_16142_b200 import configs as C
+    if scene:
+        centers, scale, albedos = C.scene_layout()
+        ms = [kaiming_uniform((5, 32, 32, 1), s) for s in range(10, 18)]
+        f = CudaNeuralField.scene(ms, centers, scale, albedos, D, bounds=C.SCENE_BOX)
+    else:
+        f = CudaNeuralField(kaiming_uniform((65, 64, 64, 1), 4), D, bounds=BOX)
+    cam = R.Camera(position=(0.3, 0.5, 3.0), look_at=(0.0, 0.1, 0.0), vfov=np.pi / 4, width=41, height=27)
+    proto = _ProtocolOnly(f)
+    for mode in ("depth", "normal", "shaded"):
+        cfg = R.RenderConfig(mode=mode, background=(0.1, 0.2, 0.3), light_dir=np.array([0.3, -2.0, 1.1]), albedo=0.6)
+        a = R.render(f, cam, cfg).data
+        b = R.render(proto, cam, cfg).data
+        if mode == "shaded":
+            np.testing.assert_allclose(a, b, rtol=0, atol=1e-15)
+        else:
+            assert np.array_equal(a, b)
+
+
+def test_device_render_mode_degenerate_normals():
+    """render.py:133-136 on the device path: a zero-gradient network (W = 0,
+    constant distance) hits every in-box pixel and every normal falls back to
+    -d, so the normal image is 0.5 * (1 - d)."""
+    m = kaiming_uniform((5, 16, 1), 0)
+    m.g[0] = np.zeros_like(m.g[0])          # W = 0: constant output, zero gradient
+    m.b[1] = np.array([0.5])
+    f = CudaNeuralField(m, D, bounds=BOX)
+    cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=9, height=7)
+    img = R.render(f, cam, R.RenderConfig(mode="normal")).data.reshape(-1, 3)
+    _, d = R.pixel_rays(cam)
+    o = np.broadcast_to(cam.position, d.shape)
+    t, hit = f.trace_batch(o, d)
+    assert hit.all()
+    assert np.array_equal(img, 0.5 * (-d + 1.0))
