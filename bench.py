@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf", "bvh", "march"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf", "bvh", "march", "modes"])
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
@@ -437,6 +437,99 @@ def bench_bvh(args, rank, world, local):
         print(json.dumps(res))
 
 
+# ----------------------------------------------------------------- single-bounce modes
+def cpu_modes(args, reference_line=False):
+    """render_depth / normal / shaded of the oracle (float64) on pixel-row bands."""
+    from oracle import cpu_ddf as O
+    W, H = 1920, 1080
+    f = oracle_field("c4")
+    cam = O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=W, height=H)
+    bands = [np.arange((y * H) // 8 * W, ((y * H) // 8 + 1) * W) for y in range(8)]
+    pix = np.concatenate(bands)
+    t0 = time.perf_counter()
+    for mode in ("depth", "normal", "shaded"):
+        O.render_mode(f, cam, mode, pixels=pix)
+    s = time.perf_counter() - t0
+    v = 3 * len(pix) / s
+    desc = f"8 pixel rows x {W} px of the 1920x1080 film per mode (depth, normal, shaded), c4 network, float64 oracle"
+    base = {"value": v, "unit": "pixels/s", "cores": cpu_cores(), "kind": "port", "sample": desc}
+    if not reference_line:
+        return base
+    return {"impl": "reference", "metric": "mode_pixels_per_s", "value": v, "unit": "pixels/s", "n_gpus": args.gpus,
+            "steps": 1, "warmup": 0, "ms_per_step": 1e3 * s, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": "modes", "sample": desc},
+            "cpu_baseline": base, "e2e": {"value": v, "unit": "pixels/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}
+
+
+def bench_modes(args, rank, world, local):
+    """render_depth / render_normal / render_shaded (render.py:144-184) at
+    1920x1080 on the c4 network (the paper's Fig. 6 t-values / normal map /
+    ray-traced), each one device call (ddf_render_mode); the same three over
+    the exact BVH mesh (Fig. 5's BVH side).  One step = the three DDF modes."""
+    import torch
+    from paper_2306_16142_b200 import configs as C
+    from paper_2306_16142_b200 import meshes as MS
+    from paper_2306_16142_b200 import render as R
+    from paper_2306_16142_b200.mesh import CudaMeshField
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    W, H = 1920, 1080
+    prec = args.precision or "bf16"
+    f = C.build_field("c4", precision=prec)
+    mesh = CudaMeshField(MS.blob(4, 0))
+    cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=W, height=H)
+    modes = ("depth", "normal", "shaded")
+
+    bufs = {m: torch.empty(W * H * (1 if m == "depth" else 3), dtype=torch.float64, device="cuda") for m in modes}
+
+    def timed(backend, mode, reps):
+        cfg = R.RenderConfig(mode=mode)
+        R.render_mode_device(backend, cam, cfg, mode, out=bufs[mode], to_host=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            R.render_mode_device(backend, cam, cfg, mode, out=bufs[mode], to_host=False)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(max(3, args.warmup)):
+        for m in modes:
+            R.render_mode_device(f, cam, R.RenderConfig(mode=m), m)
+    per = {}
+    with ClockSampler(dev) as clk:
+        for m in modes:
+            flush.zero_()
+            per[m] = timed(f, m, args.steps)
+    bvh = {m: timed(mesh, m, args.steps) for m in modes}
+    ms = sum(per.values())
+    te = []   # e2e: the public calls, image copied to the host
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for m in modes:
+            R.render(f, cam, R.RenderConfig(mode=m))
+        te.append(time.perf_counter() - t0)
+    F = C.mlp_flops(C.WORKLOADS["c4"]["widths"])
+    res = {"metric": "mode_pixels_per_s", "value": 3 * W * H / (ms / 1e3), "unit": "pixels/s", "n_gpus": world,
+           "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+           "config": {"workload": "modes", "W": W, "H": H, "network": "c4 65->8x512->1", "precision": prec,
+                      "note": "images resident on the device in value; e2e copies them to the host"},
+           "ddf_ms": per, "bvh_ms": bvh, "bvh_mesh": "blob(4, 0), 5,120 triangles",
+           "roofline": {"bound": "tensor", "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
+                        "traffic": None, "kernel": "trace step + (normal, shaded) gradient pass per pixel",
+                        "algorithmic_flops_per_step": F * W * H * 3 + 2 * F * W * H * 2},
+           "cpu_baseline": cpu_modes(args) if args.cpu_baseline else None,
+           "e2e": {"value": 3 * W * H / float(np.mean(te)), "unit": "pixels/s", "h2d_bytes_per_step": 3 * 120,
+                   "d2h_bytes_per_step": W * H * 8 * 7},
+           "gpu_launches": None, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(res))
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -498,6 +591,10 @@ def main():
             return
         print(json.dumps(cpu_queries(args, reference_line=True)))
         return
+    if args.impl == "reference" and name == "modes":
+        if rank == 0:
+            print(json.dumps(cpu_modes(args, reference_line=True)))
+        return
     if args.impl == "reference" and name == "bvh":
         if rank == 0:
             print(json.dumps(cpu_bvh(args, reference_line=True)))
@@ -543,6 +640,8 @@ def main():
         return bench_udf(args, rank, world, local)
     if name == "bvh":
         return bench_bvh(args, rank, world, local)
+    if name == "modes":
+        return bench_modes(args, rank, world, local)
 
     dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)

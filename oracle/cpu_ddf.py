@@ -604,14 +604,18 @@ def film_rgb(value, cam: Cam):
 # --------------------------------------------------------------------------
 
 def render_mode(fld: Field, cam: Cam, mode: str, background=(0.0, 0.0, 0.0),
-                light_dir=tuple(np.array([1.0, 1.0, 1.0]) / np.sqrt(3.0)), albedo=0.7, env=1.0, ambient=False):
+                light_dir=tuple(np.array([1.0, 1.0, 1.0]) / np.sqrt(3.0)), albedo=0.7, env=1.0, ambient=False,
+                pixels=None):
     """render.py:144-184: "depth" -> (H, W) t (inf on miss); "normal" /
-    "shaded" -> (H, W, 3).  Pixel-centre rays (render.py:62-63)."""
-    n = cam.width * cam.height
-    o, d = camera_rays(cam, np.full((n, 2), 0.5), np.arange(n))
+    "shaded" -> (H, W, 3).  Pixel-centre rays (render.py:62-63).  ``pixels``
+    (ascending ids) renders only that subset and returns (P,) / (P, 3)."""
+    pix = np.arange(cam.width * cam.height) if pixels is None else np.asarray(pixels, dtype=np.int64)
+    n = len(pix)
+    o, d = camera_rays(cam, np.full((n, 2), 0.5), pix)
     t, hit, obj = fld.trace(o, d)
+    shape = (cam.height, cam.width) if pixels is None else (n,)
     if mode == "depth":
-        return np.where(hit, t, np.inf).reshape(cam.height, cam.width)
+        return np.where(hit, t, np.inf).reshape(shape)
     nrm = np.zeros((n, 3))
     if hit.any():
         nrm[hit] = hit_normals(fld, o[hit], d[hit], t[hit], obj[hit])
@@ -624,7 +628,7 @@ def render_mode(fld: Field, cam: Cam, mode: str, background=(0.0, 0.0, 0.0),
     else:
         l = np.asarray(light_dir, dtype=np.float64)           # used as given (render.py:181)
         rgb[hit] = (albedo * np.maximum(nrm[hit] @ l, 0.0))[:, None]
-    return rgb.reshape(cam.height, cam.width, 3)
+    return rgb.reshape(shape + (3,))
 
 
 # --------------------------------------------------------------------------

@@ -214,10 +214,10 @@ def _device_backend(backend) -> bool:
     return getattr(backend, "handle", None) is not None and hasattr(backend, "torch_device")
 
 
-def render_mode_device(backend, camera, config, mode: str):
+def render_mode_device(backend, camera, config, mode: str, out=None, to_host: bool = True):
     """render.py:144-184 on the device (ddf_render_mode): pixel-centre rays,
     trace, hit normals and shading without host round trips.  Returns the
-    (H, W) depth or (H, W, 3) RGB array."""
+    (H, W) depth or (H, W, 3) RGB array (a device tensor with to_host=False)."""
     m = _lib.ModeConfig_t()
     m.mode = _MODE_IDS[mode]
     m.ambient = int(bool(getattr(config, "ambient", False)))
@@ -227,11 +227,14 @@ def render_mode_device(backend, camera, config, mode: str):
     m.albedo = float(config.albedo)
     m.env_radiance = float(config.env_radiance)
     W, H = camera.width, camera.height
-    out = torch.empty(W * H * (1 if mode == "depth" else 3), dtype=torch.float64, device=backend.torch_device)
+    if out is None:
+        out = torch.empty(W * H * (1 if mode == "depth" else 3), dtype=torch.float64, device=backend.torch_device)
     cam = camera_struct(camera)
     _lib.check(_lib.lib().ddf_render_mode(backend.handle, ctypes.byref(cam), ctypes.byref(m),
                                           ctypes.c_void_p(out.data_ptr()),
                                           ctypes.c_void_p(torch.cuda.current_stream(backend.torch_device).cuda_stream)))
+    if not to_host:
+        return out
     a = out.cpu().numpy()
     return a.reshape(H, W) if mode == "depth" else a.reshape(H, W, 3)
 
