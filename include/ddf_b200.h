@@ -13,13 +13,13 @@
  *    C-contiguous, float64 unless stated; (N,3) arrays are row-major xyz.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
  *    stream-ordered; ddf_render_path and ddf_render_mode synchronise the
- *    stream before returning because they report numeric errors, ddf_compact
- *    synchronises too, and ddf_udf / ddf_udf_grid synchronise the device once
+ *    stream before returning because they report numeric errors,
+ *    ddf_compact and ddf_rng_doubles synchronise too, and ddf_udf /
+ *    ddf_udf_grid synchronise the device once
  *    whenever a handle first sees a new direction count (direction table).
  *  - One call at a time per field handle (its scratch is reused); handles are
  *    independent, so concurrent calls on different handles are fine.
- *    ddf_compact and ddf_rng_doubles use process-wide scratch: one caller
- *    thread at a time.
+ *    ddf_compact uses process-wide scratch: one caller thread at a time.
  *  - Return value: DDF_OK or an error class mirroring ddfield/errors.py;
  *    ddf_last_error() holds the message (thread-local).
  */
