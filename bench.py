@@ -697,6 +697,7 @@ def main():
 
     # kernel-class breakdown (one profiled render; CUDA events on the launch stream)
     stp = step(profile=1)
+    cfg.profile = 0
     torch.cuda.synchronize()
     models = C.models(name)
     F = sum(C.mlp_flops(m.widths) for m in models) if w.get("scene") else C.mlp_flops(models[0].widths)

@@ -71,6 +71,9 @@ typedef struct {
   int64_t max_wave_paths;
   /* 1: time every kernel class with CUDA events on `stream` (stats.ms_*) */
   int32_t profile;
+  /* 1: replay the waves as a CUDA graph captured on the first call with the
+     same camera, config, accumulator and field (ignored when profile = 1) */
+  int32_t graph;
 } ddf_path_config_t;
 
 typedef struct {

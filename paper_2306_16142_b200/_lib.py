@@ -67,7 +67,7 @@ class PathConfig_t(ctypes.Structure):
                 ("rr_start", ctypes.c_int32),
                 ("rr_state", ctypes.c_uint64 * 2), ("rr_inc", ctypes.c_uint64 * 2),
                 ("tile", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32)]
+                ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32), ("graph", ctypes.c_int32)]
 
 
 class ModeConfig_t(ctypes.Structure):

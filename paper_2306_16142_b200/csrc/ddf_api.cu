@@ -34,11 +34,16 @@ int fail(int code, const std::string& msg) {
 
 int pad16(int w) { return (w + 15) / 16 * 16; }
 
+// bumped whenever any scratch buffer moves: captured render graphs hold raw
+// buffer pointers and are keyed by it
+unsigned long long g_buf_epoch = 0;
+
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaError_t ensure(size_t n) {
     if (n <= bytes) return cudaSuccess;
+    ++g_buf_epoch;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -103,6 +108,13 @@ struct ddf_field_s {
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
   Buf pix, rng, umma_masks, st_u34, st_g3;
   Buf udf_dirs, udf_vals, udf_pts, udf_best, udf_arg, udf_found, udf_list, udf_seg, udf_state;
+  // captured render_path waves (cfg->graph): replayed while the key matches
+  unsigned long long gen = 0;            // bumped by add_network / set_precision
+  cudaStream_t cap_stream = nullptr;     // private capture stream
+  cudaGraphExec_t graph_exec = nullptr;
+  std::vector<unsigned char> graph_key;
+  int graph_waves = 0;
+  uint64_t graph_launches[3] = {0, 0, 0};
   // exact mesh field (ddf_mesh_create)
   mesh::MeshDev M{};
   Buf mesh_nodes, mesh_tris, mesh_tof;
@@ -562,6 +574,7 @@ int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths
   N.wimg_fwd = img.dev;
   N.wimg_bwd = img.dev;
   f->F.n_obj += 1;
+  f->gen += 1;
   // composite as soon as there is more than one object or a transform
   bool comp = f->F.n_obj > 1;
   for (int j = 0; j < f->F.n_obj; ++j) {
@@ -577,6 +590,7 @@ int ddf_field_set_precision(ddf_field_t f, int32_t precision) {
   if (!f) return fail(DDF_EUSAGE, "null field");
   if (precision != DDF_PREC_FP32 && precision != DDF_PREC_BF16) return fail(DDF_EUSAGE, "unknown precision");
   f->F.precision = precision;
+  f->gen += 1;
   CUDA_TRY(cudaSetDevice(f->device));
   CUDA_TRY(cudaMemcpy(f->F_dev, &f->F, sizeof(FieldDev), cudaMemcpyHostToDevice));
   return DDF_OK;
@@ -594,6 +608,8 @@ int ddf_field_destroy(ddf_field_t f) {
                  &f->udf_seg, &f->udf_state, &f->mesh_nodes, &f->mesh_tris, &f->mesh_tof};
   for (Buf* b : bufs) b->release();
   if (f->F_dev) cudaFree(f->F_dev);
+  if (f->graph_exec) cudaGraphExecDestroy(f->graph_exec);
+  if (f->cap_stream) cudaStreamDestroy(f->cap_stream);
   delete f;
   return DDF_OK;
 }
@@ -815,78 +831,141 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   w.err = sm.err; w.degenerate = sm.stats + 2;
 
   int waves = 0;
-  for (int s0 = 0; s0 < cfg->spp; s0 += ns) {
-    w.s0 = s0;
-    w.ns = std::min(ns, cfg->spp - s0);
-    const int Pw = w.ns * n_own;
-    const int g = (Pw + 255) / 256;
-    {
-      ProfScope ps(f->prof, Prof::OTHER, st);
-      camera_kernel<<<g, 256, 0, st>>>(f->F, C, w, S, Pw);
-      f->prof.launches += 1;
-    }
-    CUDA_TRY(cudaGetLastError());
-    if (f->F.is_mesh) {
-      ProfScope ps(f->prof, Prof::FWD, st);
-      mesh::trace_paths_kernel<<<g, 256, 0, st>>>(f->M, S, nullptr, nullptr, Pw);
-      f->prof.launches += 1;
-      f->prof.fwd_launches += 1;
-    } else if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st)) {
-      return rc;
-    }
-    {
-      ProfScope ps(f->prof, Prof::OTHER, st);
-      after_primary_kernel<<<g, 256, 0, st>>>(w, S, Pw);
-      f->prof.launches += 1;
-    }
-    for (int b = 0; b < cfg->bounces; ++b) {
-      if (cfg->rr_start >= 0 && b >= cfg->rr_start) {
-        ProfScope ps(f->prof, Prof::OTHER, st);
-        roulette_kernel<<<g, 256, 0, st>>>(w, S, Pw, b);
-        f->prof.launches += 1;
-      }
-      int rc = compact_flags(f, S.alive, f->F.n_obj > 1 ? S.obj : nullptr, Pw, f->F.n_obj, f->list.as<int>(),
-                             sm.seg, sm.count2, sm.stats + 1, st);
-      if (rc) return rc;
-      if (f->F.is_mesh) {
-        ProfScope ps(f->prof, Prof::GRAD, st);
-        mesh::face_normal_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->M, S, f->list.as<int>(), sm.count2);
-        f->prof.launches += 1;
-        f->prof.grad_launches += 1;
-      } else {
-        GradOutOp op{};
-        op.list = f->list.as<int>(); op.count = sm.count2; op.n = Pw;
-        op.seg = f->F.n_obj > 1 ? sm.seg : nullptr;
-        op.S = S; op.backoff = f->F.backoff;
-        if ((rc = run_mlp(f, f->F, op, Pw, true, st))) return rc;
-      }
+  // the wave loop: stream-ordered launches only (no host syncs, no
+  // allocations once the buffers have grown), so it can be captured
+  auto run_waves = [&](cudaStream_t ss) -> int {
+    waves = 0;
+    for (int s0 = 0; s0 < cfg->spp; s0 += ns) {
+      w.s0 = s0;
+      w.ns = std::min(ns, cfg->spp - s0);
+      const int Pw = w.ns * n_own;
+      const int g = (Pw + 255) / 256;
       {
-        ProfScope ps(f->prof, Prof::OTHER, st);
-        bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->F_dev, w, S, f->list.as<int>(), sm.count2, b);
+        ProfScope ps(f->prof, Prof::OTHER, ss);
+        camera_kernel<<<g, 256, 0, ss>>>(f->F, C, w, S, Pw);
         f->prof.launches += 1;
       }
+      CUDA_TRY(cudaGetLastError());
       if (f->F.is_mesh) {
-        ProfScope ps(f->prof, Prof::FWD, st);
-        mesh::trace_paths_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(f->M, S, f->list.as<int>(), sm.count2,
-                                                                              Pw);
+        ProfScope ps(f->prof, Prof::FWD, ss);
+        mesh::trace_paths_kernel<<<g, 256, 0, ss>>>(f->M, S, nullptr, nullptr, Pw);
         f->prof.launches += 1;
         f->prof.fwd_launches += 1;
-      } else if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, st))) {
+      } else if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, ss)) {
         return rc;
       }
       {
-        ProfScope ps(f->prof, Prof::OTHER, st);
-        after_bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, st>>>(w, S, f->list.as<int>(), sm.count2);
+        ProfScope ps(f->prof, Prof::OTHER, ss);
+        after_primary_kernel<<<g, 256, 0, ss>>>(w, S, Pw);
         f->prof.launches += 1;
       }
+      for (int b = 0; b < cfg->bounces; ++b) {
+        if (cfg->rr_start >= 0 && b >= cfg->rr_start) {
+          ProfScope ps(f->prof, Prof::OTHER, ss);
+          roulette_kernel<<<g, 256, 0, ss>>>(w, S, Pw, b);
+          f->prof.launches += 1;
+        }
+        int rc = compact_flags(f, S.alive, f->F.n_obj > 1 ? S.obj : nullptr, Pw, f->F.n_obj, f->list.as<int>(),
+                               sm.seg, sm.count2, sm.stats + 1, ss);
+        if (rc) return rc;
+        if (f->F.is_mesh) {
+          ProfScope ps(f->prof, Prof::GRAD, ss);
+          mesh::face_normal_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(f->M, S, f->list.as<int>(), sm.count2);
+          f->prof.launches += 1;
+          f->prof.grad_launches += 1;
+        } else {
+          GradOutOp op{};
+          op.list = f->list.as<int>(); op.count = sm.count2; op.n = Pw;
+          op.seg = f->F.n_obj > 1 ? sm.seg : nullptr;
+          op.S = S; op.backoff = f->F.backoff;
+          if ((rc = run_mlp(f, f->F, op, Pw, true, ss))) return rc;
+        }
+        {
+          ProfScope ps(f->prof, Prof::OTHER, ss);
+          bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(f->F_dev, w, S, f->list.as<int>(), sm.count2, b);
+          f->prof.launches += 1;
+        }
+        if (f->F.is_mesh) {
+          ProfScope ps(f->prof, Prof::FWD, ss);
+          mesh::trace_paths_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(f->M, S, f->list.as<int>(), sm.count2,
+                                                                                Pw);
+          f->prof.launches += 1;
+          f->prof.fwd_launches += 1;
+        } else if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, ss))) {
+          return rc;
+        }
+        {
+          ProfScope ps(f->prof, Prof::OTHER, ss);
+          after_bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(w, S, f->list.as<int>(), sm.count2);
+          f->prof.launches += 1;
+        }
+      }
+      {
+        ProfScope ps(f->prof, Prof::OTHER, ss);
+        film_kernel<<<(n_own + 255) / 256, 256, 0, ss>>>(w, S, accum);
+        f->prof.launches += 1;
+      }
+      CUDA_TRY(cudaGetLastError());
+      ++waves;
     }
-    {
-      ProfScope ps(f->prof, Prof::OTHER, st);
-      film_kernel<<<(n_own + 255) / 256, 256, 0, st>>>(w, S, accum);
-      f->prof.launches += 1;
+    return DDF_OK;
+  };
+  // CUDA graph replay (cfg->graph): the captured loop is keyed by the field
+  // generation, the buffer epoch, the camera, the config and the accumulator
+  const bool use_graph = cfg->graph != 0 && !f->prof.on;
+  std::vector<unsigned char> gkey;
+  if (use_graph) {
+    ddf_path_config_t kc = *cfg;
+    kc.profile = 0;
+    kc.graph = 0;
+    const unsigned long long gen = f->gen;
+    const void* acc = accum;
+    auto put = [&](const void* p, size_t n) { gkey.insert(gkey.end(), (const unsigned char*)p, (const unsigned char*)p + n); };
+    put(&gen, sizeof gen);
+    put(cam, sizeof(*cam));
+    put(&kc, sizeof kc);
+    put(&acc, sizeof acc);
+  }
+  auto epoch_key = [&]() {
+    std::vector<unsigned char> k = gkey;
+    k.insert(k.end(), (const unsigned char*)&g_buf_epoch, (const unsigned char*)&g_buf_epoch + sizeof g_buf_epoch);
+    return k;
+  };
+  if (use_graph && f->graph_exec && f->graph_key == epoch_key()) {
+    CUDA_TRY(cudaGraphLaunch(f->graph_exec, st));
+    waves = f->graph_waves;
+    f->prof.launches = f->graph_launches[0];
+    f->prof.fwd_launches = f->graph_launches[1];
+    f->prof.grad_launches = f->graph_launches[2];
+  } else {
+    if (int rc = run_waves(st)) return rc;
+    if (use_graph) {
+      const uint64_t l0 = f->prof.launches, l1 = f->prof.fwd_launches, l2 = f->prof.grad_launches;
+      const int w0 = waves;
+      if (!f->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&f->cap_stream, cudaStreamNonBlocking));
+      if (f->graph_exec) {
+        cudaGraphExecDestroy(f->graph_exec);
+        f->graph_exec = nullptr;
+      }
+      const std::vector<unsigned char> k = epoch_key();   // the eager run grew every buffer already
+      cudaGraph_t graph = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(f->cap_stream, cudaStreamCaptureModeRelaxed));
+      const int rc = run_waves(f->cap_stream);
+      const cudaError_t ec = cudaStreamEndCapture(f->cap_stream, &graph);
+      if (rc == DDF_OK && ec == cudaSuccess && graph && k == epoch_key()) {
+        if (cudaGraphInstantiate(&f->graph_exec, graph, 0) == cudaSuccess) {
+          f->graph_key = k;
+          f->graph_waves = w0;
+          f->graph_launches[0] = l0; f->graph_launches[1] = l1; f->graph_launches[2] = l2;
+        } else {
+          f->graph_exec = nullptr;
+        }
+      }
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();   // a failed capture only means no replay next time
+      f->prof.launches = l0; f->prof.fwd_launches = l1; f->prof.grad_launches = l2;
+      waves = w0;
     }
-    CUDA_TRY(cudaGetLastError());
-    ++waves;
   }
   if (f->prof.on) f->prof.marks[Prof::TOTAL].push_back({t_begin, f->prof.rec(st)});
   int host_small[32 + 8];

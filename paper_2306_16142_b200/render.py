@@ -86,6 +86,7 @@ class RenderConfig:
     world: int = 1
     max_wave_paths: int = 0
     profile: int = 0            # 1: per-kernel-class CUDA-event timing in the stats
+    graph: int = 1              # 1: replay the waves as a captured CUDA graph (same camera/config/accumulator)
 
     def __post_init__(self):
         if self.spp < 1:
@@ -133,6 +134,7 @@ def path_struct(config) -> _lib.PathConfig_t:
     p.world = int(getattr(config, "world", 1))
     p.max_wave_paths = int(getattr(config, "max_wave_paths", 0))
     p.profile = int(getattr(config, "profile", 0))
+    p.graph = int(getattr(config, "graph", 1))
     return p
 
 
