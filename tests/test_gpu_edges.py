@@ -229,3 +229,27 @@ def test_device_render_mode_degenerate_normals():
     t, hit = f.trace_batch(o, d)
     assert hit.all()
     assert np.array_equal(img, 0.5 * (-d + 1.0))
+
+
+def test_graph_replay_identical_and_invalidated():
+    """cfg.graph: the second call with the same camera / config / accumulator
+    replays the captured waves.  Replays equal eager renders; a precision
+    change (field generation) or a scratch reallocation by another call
+    (buffer epoch) forces a fresh capture instead of a stale replay."""
+    import torch
+    f = CudaNeuralField(kaiming_uniform((5, 64, 64, 1), 9), D, bounds=BOX)
+    cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=48, height=32)
+    acc = torch.empty(48 * 32, dtype=torch.float64, device="cuda")
+    cfg = R.RenderConfig(spp=3, bounces=3, seed=4, rr_start=1, graph=1)
+    eager = R.render_path_device(f, cam, R.RenderConfig(spp=3, bounces=3, seed=4, rr_start=1, graph=0))[0].clone()
+    for _ in range(3):                                   # capture, then replays
+        assert torch.equal(R.render_path_device(f, cam, cfg, accum=acc)[0], eager)
+    f.set_precision("bf16")                              # new generation
+    bf = R.render_path_device(f, cam, R.RenderConfig(spp=3, bounces=3, seed=4, rr_start=1, graph=0))[0].clone()
+    assert not torch.equal(bf, eager)
+    assert torch.equal(R.render_path_device(f, cam, cfg, accum=acc)[0], bf)
+    big = np.random.default_rng(0).uniform(-1, 1, (300_000, 3))
+    dirs = big / np.linalg.norm(big, axis=1, keepdims=True)
+    f.trace_batch(big * 2.5, dirs)                       # grows (reallocates) the shared scratch
+    assert torch.equal(R.render_path_device(f, cam, cfg, accum=acc)[0], bf)
+    assert torch.equal(R.render_path_device(f, cam, cfg, accum=acc)[0], bf)
