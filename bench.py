@@ -29,6 +29,32 @@ sys.path.insert(0, ROOT)
 DEFAULT_CONFIG = "c4"
 
 
+def tensor_peak(prec, widths_list, long_step):
+    """Roofline denominator for the MLP engine that `prec` selects.
+
+    bf16: MEASURED_PEAKS.json's bf16 figure (sustained for kernels inside a
+    long step, burst otherwise).  fp32 on networks <= 256 wide runs 3xTF32 on
+    tcgen05: TF32 issues at half the bf16 rate (B200_PROFILING / guide table:
+    1.13 vs 2.25 PF/s) and each product costs 3 MMAs, so the ceiling for
+    algorithmic fp32 FLOPs is bf16 / 6.  fp32_simt (and fp32 on wider
+    networks) is the FFMA pipe: 148 SMs x 128 FMA/clk x 2 x max SM clock."""
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    key = "bf16_tflops_sustained" if long_step else "bf16_tflops"
+    bf16 = float(peaks[key]) if key in peaks else (1400.0 if long_step else 1590.0)
+    src = ("MEASURED_PEAKS.json " + key) if key in peaks else "fallback " + ("sustained 1.4" if long_step else "burst 1.59") + " PF/s"
+    x3 = prec == "fp32" and all(max(w[1:-1]) <= 256 and w[0] <= 96 and len(w) >= 3 for w in widths_list)
+    if prec == "bf16":
+        return bf16, src, "tensor"
+    if x3:
+        return bf16 / 6.0, src + " / 6 (3xTF32: tf32 at half the bf16 rate, 3 MMAs per product)", "tensor"
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12, "FFMA pipe: 148 SMs x 128 FMA/clk x 2 x %.0f MHz" % mhz, "fma"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -36,7 +62,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "udf", "bvh", "march", "modes"])
-    ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16"])
+    ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16", "fp32_simt"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -196,14 +222,16 @@ def bench_queries(args, rank, world, local):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     F = C.mlp_flops(w["widths"])
     ach = F * n / (ms / 1e3) / 1e12
-    peak = float(peaks.get("bf16_tflops", 1590.0))
+    peak, peak_src, bound = tensor_peak(prec, [w["widths"]], False)
     out = {"metric": "ddf_queries_per_s", "value": n / (ms / 1e3), "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
            "config": {"workload": "c1", "n": n, "widths": list(w["widths"]), "precision": prec,
                       "l2": "flushed (256 MB write) between timed steps"},
-           "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                        "traffic": None, "kernel": "fused DDF-MLP query (launch-latency bound at 65,536 rows)"},
+           "roofline": {"bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                        "traffic": None, "kernel": "fused DDF-MLP query (launch-latency bound at 65,536 rows)",
+                        "peak_source": peak_src,
+                        "frac_of_bf16_peak": ach / float(peaks.get("bf16_tflops", 1590.0))},
            "cpu_baseline": cpu_queries(args),
            "e2e": {"value": n / float(np.mean(te)), "unit": "queries/s", "h2d_bytes_per_step": 2 * n * 24,
                    "d2h_bytes_per_step": n * (8 + 8 + 1 + 4)},
@@ -233,7 +261,7 @@ def bench_queries(args, rank, world, local):
                           "tflops": F * big / (t / 1e3) / 1e12})
     out["sweep"] = sweep
     out["sweep_note"] = ("5->4x128->1: 128-wide layers cap UMMA at N = 128, about half the bf16 tensor peak "
-                         "(DESIGN.md section 3); fp32 runs on the FFMA pipe (74 TF/s peak)")
+                         "(DESIGN.md section 3); fp32 runs 3xTF32 on tcgen05 (ceiling bf16 / 6)")
     if rank == 0:
         print(json.dumps(out))
 
@@ -713,18 +741,16 @@ def main():
     # burst peak for a kernel timed alone / in a short step, the sustained
     # (power-capped) figure for kernels timed inside a long step
     long_step = ms > 1000.0
-    if peaks:
-        peak_tf = float(peaks.get("bf16_tflops_sustained" if long_step else "bf16_tflops"))
-        peak_src = ("MEASURED_PEAKS.json bf16_tflops_sustained (kernels inside a %.1f s step)" % (ms / 1e3)
-                    if long_step else "MEASURED_PEAKS.json bf16_tflops (burst)")
-    else:
-        peak_tf, peak_src = (1400.0, "fallback sustained 1.4 PF/s") if long_step else (1590.0, "fallback burst 1.59 PF/s")
+    peak_tf, peak_src, bound = tensor_peak(prec, [m.widths for m in models], long_step)
+    if long_step:
+        peak_src += " (kernels inside a %.1f s step)" % (ms / 1e3)
     achieved_tf = (fwd_flops + grad_flops) / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else 0.0
-    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+    roofline = {"bound": bound, "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved_tf / peak_tf, "traffic": None,
                 "kernel": "fused DDF-MLP (forward trace-step + input-gradient bounce)",
                 "peak_source": peak_src,
-                "frac_of_burst_peak": achieved_tf / float(peaks.get("bf16_tflops", 1590.0)),
+                "frac_of_burst_peak": achieved_tf / tensor_peak(prec, [m.widths for m in models], False)[0],
+                "frac_of_bf16_peak": achieved_tf / float(peaks.get("bf16_tflops", 1590.0)),
                 "mlp_share_of_step": mlp_ms / stp["ms_total"] if stp["ms_total"] else None,
                 "forward": {"rows": stp["forward_rows"], "ms": stp["ms_forward"], "launches": stp["forward_launches"],
                             "tflops": fwd_flops / (stp["ms_forward"] / 1e3) / 1e12 if stp["ms_forward"] else None},

@@ -37,8 +37,9 @@ extern "C" {
 #define DDF_ENUMERIC 3 /* NumericError (errors.py:16-17, exit 3)            */
 #define DDF_ECUDA 4    /* CUDA runtime failure                             */
 
-#define DDF_PREC_FP32 0 /* exact fp32 FFMA MLP                            */
-#define DDF_PREC_BF16 1 /* tcgen05 bf16 MLP, fp32 accumulate              */
+#define DDF_PREC_FP32 0      /* fp32-accurate MLP: 3xTF32 on tcgen05 (hidden <= 256 wide), else FFMA */
+#define DDF_PREC_BF16 1      /* tcgen05 bf16 MLP, fp32 accumulate              */
+#define DDF_PREC_FP32_SIMT 2 /* exact fp32 FFMA MLP (CUDA cores), any width    */
 
 #define DDF_ENC_RAW5 0  /* neural.py:26-38 (x,y,z,az/pi-1,2pol/pi-1)      */
 #define DDF_ENC_PE6 1   /* + 6-octave sin/cos encoding -> 65 inputs (configs 3-5) */

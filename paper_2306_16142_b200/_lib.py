@@ -24,7 +24,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 DDF_OK, DDF_EUSAGE, DDF_EDATA, DDF_ENUMERIC, DDF_ECUDA = 0, 1, 2, 3, 4
-PREC_FP32, PREC_BF16 = 0, 1
+PREC_FP32, PREC_BF16, PREC_FP32_SIMT = 0, 1, 2
+PRECISIONS = {"fp32": PREC_FP32, "bf16": PREC_BF16, "fp32_simt": PREC_FP32_SIMT}
 ENC_RAW5, ENC_PE6 = 0, 1
 
 EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "ddf_field_set_precision",

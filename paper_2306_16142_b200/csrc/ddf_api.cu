@@ -11,6 +11,7 @@
 #include "ddf_common.cuh"
 #include "field_kernels.cuh"
 #include "mlp_umma.cuh"
+#include "mlp_x3.cuh"
 #include "udf.cuh"
 #include "mesh.cuh"
 #include "wavefront.cuh"
@@ -101,6 +102,7 @@ struct ddf_field_s {
   FieldDev* F_dev = nullptr;    // device copy (bounce_kernel reads albedos through it)
   std::vector<void*> weights;   // device weight allocations
   std::vector<umma::NetImage> images;
+  std::vector<umma::NetImage> images_x3;   // 3xTF32 images (empty entries for networks the engine cannot take)
   int device = 0;
   int sm_count = 148;
   // scratch
@@ -181,6 +183,21 @@ int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool 
   ProfScope ps(f->prof, grad ? Prof::GRAD : Prof::FWD, st);
   f->prof.launches += 1;
   (grad ? f->prof.grad_launches : f->prof.fwd_launches) += 1;
+  // fp32 mode: the 3xTF32 tensor-core engine when every network fits it
+  bool x3 = F.precision == PREC_FP32;
+  for (int j = 0; j < F.n_obj; ++j) x3 = x3 && F.net[j].wimg_x3 != nullptr;
+  if (x3) {
+    CUDA_TRY(f->umma_masks.ensure(sizeof(uint32_t) * (size_t)umma::MASK_WORDS_PER_CTA * umma::QS * f->sm_count));
+    std::vector<umma::NetImage> imgs;
+    if (F.n_obj == 1 && f->F.n_obj > 1) {
+      for (auto& im : f->images_x3)
+        if (im.dev == F.net[0].wimg_x3) imgs.push_back(im);
+    } else {
+      imgs = f->images_x3;
+    }
+    int rc = x3::launch<Op>(F, imgs, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st, &g_err);
+    return rc ? (rc == 1 ? DDF_EUSAGE : DDF_ECUDA) : DDF_OK;
+  }
   bool tensor = F.precision == PREC_BF16;
   for (int j = 0; j < F.n_obj; ++j) tensor = tensor && F.net[j].wimg_fwd != nullptr;
   if (tensor) {
@@ -475,7 +492,8 @@ const char* ddf_last_error(void) { return g_err.c_str(); }
 int ddf_field_create(double delta, const double bounds[6], int32_t precision, int32_t device, ddf_field_t* out) {
   if (!out) return fail(DDF_EUSAGE, "null output handle");
   if (!(delta > 0.0)) return fail(DDF_EUSAGE, "delta must be positive");
-  if (precision != DDF_PREC_FP32 && precision != DDF_PREC_BF16) return fail(DDF_EUSAGE, "unknown precision");
+  if (precision != DDF_PREC_FP32 && precision != DDF_PREC_BF16 && precision != DDF_PREC_FP32_SIMT)
+    return fail(DDF_EUSAGE, "unknown precision");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(DDF_ECUDA, "no CUDA device: the B200 DDF path has no CPU fallback");
@@ -573,6 +591,15 @@ int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths
   f->images.push_back(img);
   N.wimg_fwd = img.dev;
   N.wimg_bwd = img.dev;
+  // 3xTF32 images (fp32 mode on the tensor cores) when the widths fit the engine
+  umma::NetImage img3{};
+  img3.in_width = widths[0];
+  if (x3::supports(widths, n_widths)) {
+    int rc = x3::build_image(widths, n_widths, weights, biases, &img3, &g_err);
+    if (rc) return rc;
+  }
+  f->images_x3.push_back(img3);
+  N.wimg_x3 = img3.dev;
   f->F.n_obj += 1;
   f->gen += 1;
   // composite as soon as there is more than one object or a transform
@@ -588,7 +615,8 @@ int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths
 
 int ddf_field_set_precision(ddf_field_t f, int32_t precision) {
   if (!f) return fail(DDF_EUSAGE, "null field");
-  if (precision != DDF_PREC_FP32 && precision != DDF_PREC_BF16) return fail(DDF_EUSAGE, "unknown precision");
+  if (precision != DDF_PREC_FP32 && precision != DDF_PREC_BF16 && precision != DDF_PREC_FP32_SIMT)
+    return fail(DDF_EUSAGE, "unknown precision");
   f->F.precision = precision;
   f->gen += 1;
   CUDA_TRY(cudaSetDevice(f->device));
@@ -601,6 +629,7 @@ int ddf_field_destroy(ddf_field_t f) {
   cudaSetDevice(f->device);
   for (void* p : f->weights) cudaFree(p);
   for (auto& im : f->images) umma::free_image(&im);
+  for (auto& im : f->images_x3) umma::free_image(&im);
   Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones,
                  &f->st_o, &f->st_d, &f->st_tacc, &f->st_texit, &f->st_t, &f->st_thr, &f->st_rad,
                  &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks, &f->st_u34, &f->st_g3,

@@ -146,7 +146,7 @@ __device__ __forceinline__ double pcg_single(const PcgStream& st, uint64_t k) {
 }
 
 // ---------------------------------------------------------------- network / field
-enum Precision : int { PREC_FP32 = 0, PREC_BF16 = 1 };
+enum Precision : int { PREC_FP32 = 0, PREC_BF16 = 1, PREC_FP32_SIMT = 2 };
 enum Encoding : int { ENC_RAW5 = 0, ENC_PE6 = 1 };
 
 struct NetDev {
@@ -163,6 +163,8 @@ struct NetDev {
   // bf16 tcgen05 engine: UMMA-ready pre-swizzled weight images (see mlp_umma.cuh)
   const void* wimg_fwd;
   const void* wimg_bwd;
+  // fp32 mode on the tensor cores: 3xTF32 program + images (mlp_x3.cuh), or null
+  const void* wimg_x3;
   int max_width;
 };
 

@@ -62,15 +62,15 @@ class CudaNeuralField:
                        else self.DEFAULT_BOUNDS.copy())
         self.grid_bounds = self.bounds
         self.normal_eval_backoff = 0.5 * self.delta           # field.py:237
-        if precision not in ("fp32", "bf16"):
-            raise ValueError("precision must be 'fp32' or 'bf16'")
+        if precision not in _lib.PRECISIONS:
+            raise ValueError("precision must be 'fp32', 'bf16' or 'fp32_simt'")
         self.precision = precision
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.torch_device = torch.device("cuda", self.device)
         L = _lib.lib()
         h = ctypes.c_void_p()
         b6 = (ctypes.c_double * 6)(*self.bounds.reshape(-1).tolist())
-        _lib.check(L.ddf_field_create(self.delta, b6, _lib.PREC_BF16 if precision == "bf16" else _lib.PREC_FP32,
+        _lib.check(L.ddf_field_create(self.delta, b6, _lib.PRECISIONS[precision],
                                       self.device, ctypes.byref(h)))
         self._h = h
         self.albedos = None
@@ -111,10 +111,9 @@ class CudaNeuralField:
         return self
 
     def set_precision(self, precision: str) -> None:
-        if precision not in ("fp32", "bf16"):
-            raise ValueError("precision must be 'fp32' or 'bf16'")
-        _lib.check(_lib.lib().ddf_field_set_precision(
-            self._h, _lib.PREC_BF16 if precision == "bf16" else _lib.PREC_FP32))
+        if precision not in _lib.PRECISIONS:
+            raise ValueError("precision must be 'fp32', 'bf16' or 'fp32_simt'")
+        _lib.check(_lib.lib().ddf_field_set_precision(self._h, _lib.PRECISIONS[precision]))
         self.precision = precision
 
     def __del__(self):
