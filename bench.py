@@ -209,6 +209,7 @@ def bench_queries(args, rank, world, local):
             e1.record(st)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+        clk.top_up(step)
     ms = float(np.mean(times))
     # e2e through the public protocol call (numpy in, numpy out)
     f.query_raw(o, d)
@@ -335,6 +336,7 @@ def bench_udf(args, rank, world, local):
             e1.record(st)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+        clk.top_up(step)
     ms = float(np.mean(times))
     te = []
     for _ in range(args.steps):
@@ -436,6 +438,7 @@ def bench_bvh(args, rank, world, local):
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+        clk.top_up(lambda: R.render_path_device(fld, cam, cfg, accum=accum, stream=stream))
     ms = float(np.mean(times))
     cfg.profile = 1
     _, prof = R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
@@ -531,6 +534,7 @@ def bench_modes(args, rank, world, local):
         for m in modes:
             flush.zero_()
             per[m] = timed(f, m, args.steps)
+        clk.top_up(lambda: [R.render_mode_device(f, cam, R.RenderConfig(mode=m), m) for m in modes])
     bvh = {m: timed(mesh, m, args.steps) for m in modes}
     ms = sum(per.values())
     te = []   # e2e: the public calls, image copied to the host
@@ -576,9 +580,27 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a moment to start: wait for its first row so the
+            # sampler is live when the timed region begins
+            t_end = time.perf_counter() + 3.0
+            while not self.rows and time.perf_counter() < t_end:
+                time.sleep(0.01)
+            self.start = len(self.rows)
         except Exception:
             self.proc = None
+        self.extended_s = 0.0
         return self
+
+    def top_up(self, fn, min_samples=3, max_s=3.0):
+        """A timed region shorter than the 100 ms sample period may see no
+        sample: keep the same work running (untimed) until a few samples
+        land, and say so in the summary."""
+        import torch
+        t0 = time.perf_counter()
+        while self.proc and len(self.rows) - self.start < min_samples and time.perf_counter() - t0 < max_s:
+            fn()
+            torch.cuda.synchronize()
+        self.extended_s = time.perf_counter() - t0 if len(self.rows) - self.start else 0.0
 
     def _read(self):
         for line in self.proc.stdout:
@@ -593,17 +615,22 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        rows = self.rows[getattr(self, "start", 0):] or self.rows
+        sm = [float(r[0]) for r in rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for r in rows:
             if len(r) >= 8:
                 for nm, v in zip(names, r[4:8]):
                     if v.lower() == "active":
                         reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": sorted(reasons), "samples": len(rows)}
+        if self.extended_s > 0.05:
+            out["note"] = ("timed region shorter than the 100 ms sample period: sampled while the same step "
+                           "kept running untimed for %.2f s after it" % self.extended_s)
+        return out
 
 
 # ----------------------------------------------------------------- GPU side
@@ -715,6 +742,8 @@ def main():
             torch.cuda.synchronize()
             per_step.append(e0.elapsed_time(e1))
             launches += st["kernel_launches"]
+        # rank-local work only (no collective: ranks may top up a different number of times)
+        clk.top_up(lambda: R.render_path_device(fld, cam, cfg, accum=accum, stream=stream))
     ms_local = float(np.mean(per_step))
     t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
     if world > 1:
