@@ -760,8 +760,13 @@ def main():
     F = sum(C.mlp_flops(m.widths) for m in models) if w.get("scene") else C.mlp_flops(models[0].widths)
     F_grad = 2 * C.mlp_flops(models[0].widths)   # one object's network per gradient row
     fwd_flops = F * stp["forward_rows"]
-    grad_flops = F_grad * stp["gradient_rows"]
-    mlp_ms = stp["ms_forward"] + stp["ms_gradient"]
+    # executed work: the separate gradient pass runs gradient_rows_executed
+    # rows (2F each); fused trace+gradient rows add a backward chain (F) on
+    # top of their forward, which forward_rows already counts
+    grad_flops = F_grad * stp["gradient_rows_executed"]
+    fused_flops = (F_grad // 2) * stp["fused_rows"]
+    ref_flops = fwd_flops + F_grad * stp["gradient_rows"]
+    mlp_ms = stp["ms_forward"] + stp["ms_gradient"] + stp["ms_fused"]
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -773,7 +778,7 @@ def main():
     peak_tf, peak_src, bound = tensor_peak(prec, [m.widths for m in models], long_step)
     if long_step:
         peak_src += " (kernels inside a %.1f s step)" % (ms / 1e3)
-    achieved_tf = (fwd_flops + grad_flops) / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else 0.0
+    achieved_tf = (fwd_flops + grad_flops + fused_flops) / (mlp_ms / 1e3) / 1e12 if mlp_ms > 0 else 0.0
     roofline = {"bound": bound, "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved_tf / peak_tf, "traffic": None,
                 "kernel": "fused DDF-MLP (forward trace-step + input-gradient bounce)",
@@ -781,11 +786,19 @@ def main():
                 "frac_of_burst_peak": achieved_tf / tensor_peak(prec, [m.widths for m in models], False)[0],
                 "frac_of_bf16_peak": achieved_tf / float(peaks.get("bf16_tflops", 1590.0)),
                 "mlp_share_of_step": mlp_ms / stp["ms_total"] if stp["ms_total"] else None,
-                "forward": {"rows": stp["forward_rows"], "ms": stp["ms_forward"], "launches": stp["forward_launches"],
-                            "tflops": fwd_flops / (stp["ms_forward"] / 1e3) / 1e12 if stp["ms_forward"] else None},
-                "gradient": {"rows": stp["gradient_rows"], "ms": stp["ms_gradient"],
+                "forward": {"rows": stp["forward_rows"] - stp["fused_rows"], "ms": stp["ms_forward"],
+                            "launches": stp["forward_launches"],
+                            "tflops": F * (stp["forward_rows"] - stp["fused_rows"]) / (stp["ms_forward"] / 1e3) / 1e12
+                            if stp["ms_forward"] else None},
+                "gradient": {"rows": stp["gradient_rows_executed"], "ms": stp["ms_gradient"],
                              "launches": stp["gradient_launches"],
                              "tflops": grad_flops / (stp["ms_gradient"] / 1e3) / 1e12 if stp["ms_gradient"] else None},
+                "fused_trace_gradient": {
+                    "rows": stp["fused_rows"], "ms": stp["ms_fused"], "launches": stp["fused_launches"],
+                    "tflops": (F * stp["fused_rows"] + fused_flops) / (stp["ms_fused"] / 1e3) / 1e12
+                    if stp["ms_fused"] else None,
+                    "note": "bounce-ray march step 0 + the next bounce's normal gradient in one kernel where the "
+                            "inputs coincide (SURVEY 8(d) fused normal reuse): forward F + backward F per row"},
                 "compaction_ms": stp["ms_compact"], "other_ms": stp["ms_other"], "profiled_step_ms": stp["ms_total"]}
     # wavefront compaction against HBM: per compaction call the
     # flags are read twice (plus 4 B object ids twice when bucketed) and 4 B
@@ -858,7 +871,8 @@ def main():
                        "l2": "flushed (256 MB write) between timed steps"},
             "ddf_queries_per_s": stp["forward_rows"] / (ms / 1e3),
             "gradient_rows_per_s": stp["gradient_rows"] / (ms / 1e3),
-            "flops_per_step": fwd_flops + grad_flops,
+            "flops_per_step": fwd_flops + grad_flops + fused_flops,
+            "reference_equivalent_flops_per_step": ref_flops,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
         }

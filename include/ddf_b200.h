@@ -75,6 +75,10 @@ typedef struct {
   /* 1: replay the waves as a CUDA graph captured on the first call with the
      same camera, config, accumulator and field (ignored when profile = 1) */
   int32_t graph;
+  /* 1: never fuse a bounce ray's first march step with the next bounce's
+     normal gradient (0 = fuse where the engine and regime allow; results
+     are identical either way) */
+  int32_t no_fuse;
 } ddf_path_config_t;
 
 typedef struct {
@@ -97,6 +101,13 @@ typedef struct {
   uint64_t forward_launches, gradient_launches;
   /* profile = 1 only: summed CUDA-event durations per kernel class */
   double ms_forward, ms_gradient, ms_compact, ms_other, ms_total;
+  /* fused normal reuse: rows of the fused trace+gradient
+     kernel (each a forward plus a backward chain), rows of the separate
+     gradient pass actually executed (= gradient_rows when fusion is off; the
+     reference's count of normal evaluations stays in gradient_rows), that
+     kernel's launches and (profile = 1) time */
+  uint64_t fused_rows, gradient_rows_executed, fused_launches;
+  double ms_fused;
 } ddf_render_stats_t;
 
 /* NeuralField.__init__ (field.py:231-237): delta, AABB bounds (lo xyz, hi xyz). */

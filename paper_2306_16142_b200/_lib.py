@@ -68,7 +68,8 @@ class PathConfig_t(ctypes.Structure):
                 ("rr_start", ctypes.c_int32),
                 ("rr_state", ctypes.c_uint64 * 2), ("rr_inc", ctypes.c_uint64 * 2),
                 ("tile", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32), ("graph", ctypes.c_int32)]
+                ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32), ("graph", ctypes.c_int32),
+                ("no_fuse", ctypes.c_int32)]
 
 
 class ModeConfig_t(ctypes.Structure):
@@ -82,7 +83,9 @@ class RenderStats_t(ctypes.Structure):
                 ("waves", ctypes.c_int32), ("kernel_launches", ctypes.c_uint64),
                 ("forward_launches", ctypes.c_uint64), ("gradient_launches", ctypes.c_uint64),
                 ("ms_forward", ctypes.c_double), ("ms_gradient", ctypes.c_double),
-                ("ms_compact", ctypes.c_double), ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double)]
+                ("ms_compact", ctypes.c_double), ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("fused_rows", ctypes.c_uint64), ("gradient_rows_executed", ctypes.c_uint64),
+                ("fused_launches", ctypes.c_uint64), ("ms_fused", ctypes.c_double)]
 
 
 _lib = None

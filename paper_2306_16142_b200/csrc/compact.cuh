@@ -19,12 +19,15 @@ constexpr int NT = 256;
 constexpr int IPT = 4;
 constexpr int BLOCK_ITEMS = NT * IPT;
 
-__device__ __forceinline__ bool take(const uint8_t* flags, const int* obj, int idx, int n, int j) {
-  return idx < n && flags[idx] && (obj == nullptr || obj[idx] == j);
+// sel (nullable): only slots whose sel byte equals sel_val are taken
+__device__ __forceinline__ bool take(const uint8_t* flags, const uint8_t* sel, int sel_val, const int* obj, int idx,
+                                     int n, int j) {
+  return idx < n && flags[idx] && (sel == nullptr || sel[idx] == sel_val) && (obj == nullptr || obj[idx] == j);
 }
 
-__global__ void __launch_bounds__(NT) count_kernel(const uint8_t* __restrict__ flags, const int* __restrict__ obj,
-                                                   int n, int n_obj, int* __restrict__ block_counts) {
+__global__ void __launch_bounds__(NT) count_kernel(const uint8_t* __restrict__ flags, const uint8_t* __restrict__ sel,
+                                                   int sel_val, const int* __restrict__ obj, int n, int n_obj,
+                                                   int* __restrict__ block_counts) {
   __shared__ int cnt[DDF_MAX_OBJECTS];
   if (threadIdx.x < DDF_MAX_OBJECTS) cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -34,7 +37,7 @@ __global__ void __launch_bounds__(NT) count_kernel(const uint8_t* __restrict__ f
     int c = 0;
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
-      const unsigned b = __ballot_sync(0xffffffffu, take(flags, obj, base + i * NT + threadIdx.x, n, j));
+      const unsigned b = __ballot_sync(0xffffffffu, take(flags, sel, sel_val, obj, base + i * NT + threadIdx.x, n, j));
       c += __popc(b);
     }
     if (lane == 0 && c) atomicAdd(&cnt[j], c);
@@ -46,7 +49,8 @@ __global__ void __launch_bounds__(NT) count_kernel(const uint8_t* __restrict__ f
 // one CTA of 1024 threads; block_counts -> block offsets (in place)
 __global__ void __launch_bounds__(1024) scan_kernel(int* __restrict__ block_counts, int nblocks, int n_obj,
                                                     int* __restrict__ seg, int* __restrict__ count,
-                                                    unsigned long long* __restrict__ rows_acc) {
+                                                    unsigned long long* __restrict__ rows_acc,
+                                                    unsigned long long* __restrict__ rows_acc2) {
   __shared__ int part[1024];
   __shared__ int seg_base;
   if (threadIdx.x == 0) seg_base = 0;
@@ -81,10 +85,12 @@ __global__ void __launch_bounds__(1024) scan_kernel(int* __restrict__ block_coun
     seg[n_obj] = seg_base;
     *count = seg_base;
     if (rows_acc) *rows_acc += (unsigned long long)seg_base;
+    if (rows_acc2) *rows_acc2 += (unsigned long long)seg_base;
   }
 }
 
-__global__ void __launch_bounds__(NT) scatter_kernel(const uint8_t* __restrict__ flags, const int* __restrict__ obj,
+__global__ void __launch_bounds__(NT) scatter_kernel(const uint8_t* __restrict__ flags, const uint8_t* __restrict__ sel,
+                                                     int sel_val, const int* __restrict__ obj,
                                                      int n, int n_obj, const int* __restrict__ block_offsets,
                                                      int* __restrict__ list) {
   __shared__ int warp_cnt[NT / 32];
@@ -95,7 +101,7 @@ __global__ void __launch_bounds__(NT) scatter_kernel(const uint8_t* __restrict__
     int run = block_offsets[blockIdx.x * n_obj + j];
     for (int i = 0; i < IPT; ++i) {
       const int idx = base + i * NT + threadIdx.x;
-      const bool t = take(flags, obj, idx, n, j);
+      const bool t = take(flags, sel, sel_val, obj, idx, n, j);
       const unsigned b = __ballot_sync(0xffffffffu, t);
       if (lane == 0) warp_cnt[warp] = __popc(b);
       __syncthreads();

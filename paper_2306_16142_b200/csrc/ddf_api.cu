@@ -64,17 +64,17 @@ struct Buf {
 
 // Per-call kernel-class timing (cfg->profile) and launch counting.
 struct Prof {
-  enum { FWD = 0, GRAD = 1, COMPACT = 2, OTHER = 3, TOTAL = 4, NCAT = 5 };
+  enum { FWD = 0, GRAD = 1, COMPACT = 2, OTHER = 3, TOTAL = 4, FUSED = 5, NCAT = 6 };
   bool on = false;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   std::vector<std::pair<size_t, size_t>> marks[NCAT];
-  uint64_t launches = 0, fwd_launches = 0, grad_launches = 0;
+  uint64_t launches = 0, fwd_launches = 0, grad_launches = 0, fused_launches = 0;
   void reset(bool enable) {
     on = enable;
     used = 0;
     for (auto& m : marks) m.clear();
-    launches = fwd_launches = grad_launches = 0;
+    launches = fwd_launches = grad_launches = fused_launches = 0;
   }
   size_t rec(cudaStream_t st) {
     if (used == pool.size()) {
@@ -108,7 +108,7 @@ struct ddf_field_s {
   // scratch
   Buf t_acc, t_exit, alive, list, list2, blocks, small, ones;
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
-  Buf pix, rng, umma_masks, st_u34, st_g3;
+  Buf pix, rng, umma_masks, st_u34, st_g3, st_gdone, st_want;
   Buf udf_dirs, udf_vals, udf_pts, udf_best, udf_arg, udf_found, udf_list, udf_seg, udf_state;
   // captured render_path waves (cfg->graph): replayed while the key matches
   unsigned long long gen = 0;            // bumped by add_network / set_precision
@@ -116,7 +116,7 @@ struct ddf_field_s {
   cudaGraphExec_t graph_exec = nullptr;
   std::vector<unsigned char> graph_key;
   int graph_waves = 0;
-  uint64_t graph_launches[3] = {0, 0, 0};
+  uint64_t graph_launches[4] = {0, 0, 0, 0};
   // exact mesh field (ddf_mesh_create)
   mesh::MeshDev M{};
   Buf mesh_nodes, mesh_tris, mesh_tof;
@@ -127,7 +127,10 @@ struct ddf_field_s {
 
 namespace {
 
-// small scratch layout: [0..15] seg, [16] count, [17] count2, [18..19] err, u64 stats after 32 ints
+// small scratch layout: [0..15] seg, [16] count, [17] count2, [18..19] err, u64 stats after 32 ints:
+// [0] forward rows, [1] gradient rows (reference count: rows needing a normal),
+// [2] degenerate normals, [3] fused trace+gradient rows, [4] rows of the
+// gradient pass proper when fusion is on
 struct Small {
   int* seg; int* count; int* count2; int* err; unsigned long long* stats;  // stats[0]=fwd [1]=grad [2]=degenerate
 };
@@ -219,18 +222,43 @@ int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool 
   return fail(DDF_EUSAGE, "fp32 engine supports layer widths up to 512");
 }
 
+// Fused trace step + input gradient (TraceGradOp, wavefront.cuh) on the
+// bf16 tcgen05 engine: one network wider than 256, single-step march regime
+// (0.9 delta covers the box diagonal, so a bounce ray's step-0 input is where
+// its normal will be evaluated).  Anything else keeps the unfused passes.
+bool fusion_ok(const ddf_field_s* f) {
+  const FieldDev& F = f->F;
+  if (F.is_mesh || F.n_obj != 1 || F.composite || F.precision != PREC_BF16) return false;
+  if (f->images.size() != 1 || !f->images[0].dev || f->images[0].host.pp) return false;
+  double d2 = 0.0;
+  for (int k = 0; k < 3; ++k) d2 += (F.hi[k] - F.lo[k]) * (F.hi[k] - F.lo[k]);
+  return F.step >= std::sqrt(d2);
+}
+
+int run_fused(ddf_field_s* f, const TraceGradOp& op, int max_rows, cudaStream_t st) {
+  if (max_rows <= 0) return DDF_OK;
+  ProfScope ps(f->prof, Prof::FUSED, st);
+  f->prof.launches += 1;
+  f->prof.fused_launches += 1;
+  CUDA_TRY(f->umma_masks.ensure(sizeof(uint32_t) * (size_t)umma::MASK_WORDS_PER_CTA * umma::QS * f->sm_count));
+  int rc = umma::launch<TraceGradOp>(f->F, f->images, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st,
+                                     &g_err);
+  return rc ? (rc == 1 ? DDF_EUSAGE : DDF_ECUDA) : DDF_OK;
+}
+
 // stable compaction flags -> list (+ segments by object when obj != nullptr)
 int compact_flags(ddf_field_s* f, const uint8_t* flags, const int* obj, int n, int n_obj, int* list, int* seg,
-                  int* count, unsigned long long* rows_acc, cudaStream_t st) {
+                  int* count, unsigned long long* rows_acc, cudaStream_t st, const uint8_t* sel = nullptr,
+                  int sel_val = 0, unsigned long long* rows_acc2 = nullptr) {
   const int nb = std::max(1, (n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS);
   CUDA_TRY(f->blocks.ensure(sizeof(int) * nb * DDF_MAX_OBJECTS));
   int* bc = f->blocks.as<int>();
   const int no = obj ? n_obj : 1;
   ProfScope ps(f->prof, Prof::COMPACT, st);
   f->prof.launches += 3;
-  compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, obj, n, no, bc);
-  compact::scan_kernel<<<1, 1024, 0, st>>>(bc, nb, no, seg, count, rows_acc);
-  compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, obj, n, no, bc, list);
+  compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, sel, sel_val, obj, n, no, bc);
+  compact::scan_kernel<<<1, 1024, 0, st>>>(bc, nb, no, seg, count, rows_acc, rows_acc2);
+  compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, sel, sel_val, obj, n, no, bc, list);
   CUDA_TRY(cudaGetLastError());
   return DDF_OK;
 }
@@ -251,10 +279,22 @@ __global__ void trace_init_kernel(const FieldDev F, MarchState S, int n) {
 }
 
 // sphere march over the slots whose `march` flag is set (field.py:274-288)
-int march(ddf_field_s* f, const MarchState& ms, int n, int* list, unsigned long long* fwd_acc, cudaStream_t st) {
+// fused (nullable): step 0 of the rows whose `want` byte is set runs as
+// TraceGradOp (fused normal reuse); the other rows take the plain step
+int march(ddf_field_s* f, const MarchState& ms, int n, int* list, unsigned long long* fwd_acc, cudaStream_t st,
+          const TraceGradOp* fused = nullptr, const uint8_t* want = nullptr) {
   Small sm = small_of(f);
   for (int step = 0; step < f->F.max_steps; ++step) {
-    int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st);
+    const bool fz = fused && step == 0;
+    if (fz) {
+      int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st, want, 1, sm.stats + 3);
+      if (rc) return rc;
+      TraceGradOp op = *fused;
+      op.list = list; op.count = sm.count; op.n = n; op.seg = nullptr;
+      op.st = ms; op.delta = f->F.delta; op.thresh = f->F.thresh; op.step = f->F.step;
+      if ((rc = run_fused(f, op, n, st))) return rc;
+    }
+    int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st, fz ? want : nullptr, 0);
     if (rc) return rc;
     TraceStepOp op{};
     op.list = list; op.count = sm.count; op.n = n; op.seg = nullptr;
@@ -632,7 +672,7 @@ int ddf_field_destroy(ddf_field_t f) {
   for (auto& im : f->images_x3) umma::free_image(&im);
   Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones,
                  &f->st_o, &f->st_d, &f->st_tacc, &f->st_texit, &f->st_t, &f->st_thr, &f->st_rad,
-                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks, &f->st_u34, &f->st_g3,
+                 &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks, &f->st_u34, &f->st_g3, &f->st_gdone, &f->st_want,
                  &f->udf_dirs, &f->udf_vals, &f->udf_pts, &f->udf_best, &f->udf_arg, &f->udf_found, &f->udf_list,
                  &f->udf_seg, &f->udf_state, &f->mesh_nodes, &f->mesh_tris, &f->mesh_tof};
   for (Buf* b : bufs) b->release();
@@ -832,6 +872,8 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   CUDA_TRY(f->st_obj.ensure(sizeof(int) * P));
   CUDA_TRY(f->st_u34.ensure(sizeof(double) * 2 * P));
   CUDA_TRY(f->st_g3.ensure(sizeof(double) * 3 * P));
+  CUDA_TRY(f->st_gdone.ensure(P));
+  CUDA_TRY(f->st_want.ensure(P));
   CUDA_TRY(f->list.ensure(sizeof(int) * P));
   CUDA_TRY(f->list2.ensure(sizeof(int) * P));
 
@@ -843,6 +885,11 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   S.obj = f->st_obj.as<int>();
   S.u34 = f->st_u34.as<double>();
   S.g3 = f->st_g3.as<double>();
+  S.gdone = f->st_gdone.as<uint8_t>();
+  S.want = f->st_want.as<uint8_t>();
+  const bool fuse = !cfg->no_fuse && fusion_ok(f);
+  TraceGradOp tg{};
+  tg.backoff = f->F.backoff; tg.g3 = S.g3; tg.gdone = S.gdone;
   MarchState ms{};
   ms.o = S.o; ms.d = S.d; ms.t_acc = S.t_acc; ms.t_exit = S.t_exit; ms.alive = S.march;
   ms.t_out = S.t; ms.hit = S.hit; ms.obj = S.obj; ms.u34 = S.u34;
@@ -902,6 +949,15 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
           mesh::face_normal_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(f->M, S, f->list.as<int>(), sm.count2);
           f->prof.launches += 1;
           f->prof.grad_launches += 1;
+        } else if (fuse) {
+          // rows whose normal gradient the fused trace step already produced are left out
+          if ((rc = compact_flags(f, S.alive, nullptr, Pw, 1, f->list2.as<int>(), sm.seg, sm.count, sm.stats + 4, ss,
+                                  S.gdone, 0)))
+            return rc;
+          GradOutOp op{};
+          op.list = f->list2.as<int>(); op.count = sm.count; op.n = Pw; op.seg = nullptr;
+          op.S = S; op.backoff = f->F.backoff;
+          if ((rc = run_mlp(f, f->F, op, Pw, true, ss))) return rc;
         } else {
           GradOutOp op{};
           op.list = f->list.as<int>(); op.count = sm.count2; op.n = Pw;
@@ -920,7 +976,8 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
                                                                                 Pw);
           f->prof.launches += 1;
           f->prof.fwd_launches += 1;
-        } else if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, ss))) {
+        } else if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, ss,
+                               fuse && b + 1 < cfg->bounces ? &tg : nullptr, S.want))) {
           return rc;
         }
         {
@@ -966,10 +1023,12 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     f->prof.launches = f->graph_launches[0];
     f->prof.fwd_launches = f->graph_launches[1];
     f->prof.grad_launches = f->graph_launches[2];
+    f->prof.fused_launches = f->graph_launches[3];
   } else {
     if (int rc = run_waves(st)) return rc;
     if (use_graph) {
-      const uint64_t l0 = f->prof.launches, l1 = f->prof.fwd_launches, l2 = f->prof.grad_launches;
+      const uint64_t l0 = f->prof.launches, l1 = f->prof.fwd_launches, l2 = f->prof.grad_launches,
+                     l3 = f->prof.fused_launches;
       const int w0 = waves;
       if (!f->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&f->cap_stream, cudaStreamNonBlocking));
       if (f->graph_exec) {
@@ -985,25 +1044,29 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
         if (cudaGraphInstantiate(&f->graph_exec, graph, 0) == cudaSuccess) {
           f->graph_key = k;
           f->graph_waves = w0;
-          f->graph_launches[0] = l0; f->graph_launches[1] = l1; f->graph_launches[2] = l2;
+          f->graph_launches[0] = l0; f->graph_launches[1] = l1; f->graph_launches[2] = l2; f->graph_launches[3] = l3;
         } else {
           f->graph_exec = nullptr;
         }
       }
       if (graph) cudaGraphDestroy(graph);
       cudaGetLastError();   // a failed capture only means no replay next time
-      f->prof.launches = l0; f->prof.fwd_launches = l1; f->prof.grad_launches = l2;
+      f->prof.launches = l0; f->prof.fwd_launches = l1; f->prof.grad_launches = l2; f->prof.fused_launches = l3;
       waves = w0;
     }
   }
   if (f->prof.on) f->prof.marks[Prof::TOTAL].push_back({t_begin, f->prof.rec(st)});
-  int host_small[32 + 8];
+  int host_small[32 + 10];
   CUDA_TRY(cudaMemcpyAsync(host_small, f->small.p, sizeof(host_small), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   const unsigned long long* hs64 = reinterpret_cast<const unsigned long long*>(host_small + 32);
   if (stats) {
     stats->forward_rows = hs64[0];
     stats->gradient_rows = hs64[1];
+    stats->fused_rows = fuse ? hs64[3] : 0;
+    stats->gradient_rows_executed = fuse ? hs64[4] : hs64[1];
+    stats->fused_launches = f->prof.fused_launches;
+    stats->ms_fused = f->prof.total_ms(Prof::FUSED);
     stats->degenerate = hs64[2];
     stats->path_samples = (uint64_t)n_own * cfg->spp;
     stats->waves = waves;
@@ -1044,6 +1107,8 @@ int ddf_render_mode(ddf_field_t f, const ddf_camera_t* cam, const ddf_mode_confi
   CUDA_TRY(f->st_obj.ensure(sizeof(int) * P));
   CUDA_TRY(f->st_u34.ensure(sizeof(double) * 2 * P));
   CUDA_TRY(f->st_g3.ensure(sizeof(double) * 3 * P));
+  CUDA_TRY(f->st_gdone.ensure(P));
+  CUDA_TRY(f->st_want.ensure(P));
   CUDA_TRY(f->list.ensure(sizeof(int) * P));
   CUDA_TRY(f->list2.ensure(sizeof(int) * P));
   PathState S{};
@@ -1144,9 +1209,9 @@ int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, 
   const int nb = std::max<int>(1, (int)((n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS));
   CUDA_TRY(g_cs.blocks.ensure(sizeof(int) * nb));
   CUDA_TRY(g_cs.seg.ensure(sizeof(int) * 2));
-  compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, (int)n, 1, g_cs.blocks.as<int>());
-  compact::scan_kernel<<<1, 1024, 0, st>>>(g_cs.blocks.as<int>(), nb, 1, g_cs.seg.as<int>(), count, nullptr);
-  compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, (int)n, 1, g_cs.blocks.as<int>(), list);
+  compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, 0, nullptr, (int)n, 1, g_cs.blocks.as<int>());
+  compact::scan_kernel<<<1, 1024, 0, st>>>(g_cs.blocks.as<int>(), nb, 1, g_cs.seg.as<int>(), count, nullptr, nullptr);
+  compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, 0, nullptr, (int)n, 1, g_cs.blocks.as<int>(), list);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
   return DDF_OK;

@@ -71,6 +71,7 @@ __device__ __forceinline__ void st3(double* a, int64_t i, d3 v) { a[3 * i] = v.x
 
 // ---------------------------------------------------------------- row ops
 struct ListBase {
+  static constexpr bool kFused = false;   // true: trace step + input gradient in one pass (TraceGradOp)
   const int* list;      // slot ids (nullptr = identity)
   const int* count;     // device count (nullptr = n)
   int n;

@@ -58,8 +58,13 @@ constexpr int EPI_WARP0 = 2;
 constexpr int N_EPI_WARPS = 8;
 constexpr int MASK_WORDS_PER_CTA = DDF_MAX_LAYERS * 16 * ROWS;   // u32: [layer][col/32][row]
 
-enum Epi : int { E_RELU_A = 0, E_HEAD = 1, E_RELU_MASK_A = 2, E_MASKG_A = 3, E_BWD_MASK_A = 4, E_BWD_OUT = 5 };
-__host__ __device__ inline bool writes_a(int e) { return e == E_RELU_A || e == E_RELU_MASK_A || e == E_MASKG_A || e == E_BWD_MASK_A; }
+// E_MASKG_HEAD_A exists only inside fused trace+gradient kernels (Op::kFused):
+// the gradient program's E_MASKG_A step that also forms the identity head.
+enum Epi : int { E_RELU_A = 0, E_HEAD = 1, E_RELU_MASK_A = 2, E_MASKG_A = 3, E_BWD_MASK_A = 4, E_BWD_OUT = 5,
+                 E_MASKG_HEAD_A = 6 };
+__host__ __device__ inline bool writes_a(int e) {
+  return e == E_RELU_A || e == E_RELU_MASK_A || e == E_MASKG_A || e == E_BWD_MASK_A || e == E_MASKG_HEAD_A;
+}
 
 struct __align__(16) Step {
   int K, N, nh, epi;
@@ -210,7 +215,8 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
                                            uint32_t* my_masks, const float* head_w, float& head_part,
                                            uint32_t bar_free, uint32_t& free_ph, const float* sparams,
                                            const uint32_t (&mpre)[4]) {
-  constexpr bool WA = EPI == E_RELU_A || EPI == E_RELU_MASK_A || EPI == E_MASKG_A || EPI == E_BWD_MASK_A;
+  constexpr bool WA = EPI == E_RELU_A || EPI == E_RELU_MASK_A || EPI == E_MASKG_A || EPI == E_BWD_MASK_A ||
+                     EPI == E_MASKG_HEAD_A;
   constexpr bool BIAS = EPI != E_BWD_MASK_A;
   constexpr int HOLD = NM < 2 ? NM : 2;
   const int r7 = r & 7;
@@ -271,6 +277,13 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
   #pragma unroll
           for (int e = 0; e < 32; e += 4) {
             const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+            if constexpr (EPI == E_MASKG_HEAD_A) {
+              // the identity head of the forward, in E_HEAD's order (same fp32 result)
+              head_part = fmaf(v[e], hw.x, head_part);
+              head_part = fmaf(v[e + 1], hw.y, head_part);
+              head_part = fmaf(v[e + 2], hw.z, head_part);
+              head_part = fmaf(v[e + 3], hw.w, head_part);
+            }
             v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
             v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
             v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
@@ -319,6 +332,7 @@ __device__ __forceinline__ void epi_half(int nmine, const Step& st, int c_first,
     case 0: epi_chunks<EPI, 0>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
     case 1: epi_chunks<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
     case 2: epi_chunks<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    case 3: epi_chunks<EPI, 3>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
     default: epi_chunks<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
   }
 }
@@ -458,6 +472,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int a_bytes,
            int stage_bytes, int params_bytes, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // fused trace+gradient (Op::kFused): the gradient program, whose last
+  // forward epilogue also forms the head and hands the distance to the row op
+  constexpr bool kProgG = Op::kGrad || Op::kFused;
   uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem S;
   S.a = base_ptr;
@@ -513,10 +530,10 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
         tile_rows(F, op, t, j0, j1, base, nv);
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
-          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
-          const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
+          const int ns = __ldg(kProgG ? &P->n_grad : &P->n_fwd);
+          const uint8_t* img = kProgG ? P->img_grad : P->img_fwd;
           for (int s = 0; s < ns; ++s) {
-            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
             const uint8_t* src = img + st.img_off;
             const int nck = st.nh * st.nchunk;
             for (int c = 0; c < nck; ++c) {
@@ -550,10 +567,10 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
         tile_rows(F, op, t, j0, j1, base, nv);
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
-          const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
+          const int ns = kProgG ? P->n_grad : P->n_fwd;
           int prev_rows = 1 << 30;
           for (int s = 0; s < ns; ++s) {
-            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
             const uint32_t id = idesc(st.rows);
             const bool wa = writes_a(st.epi);
             const int c0 = min(st.nchunk - 1, ((st.N >> 1) - 1) >> 6);   // last chunk touching A cols < N/2
@@ -664,10 +681,10 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
         __syncwarp();
         if (lane == 0) { mbar_arrive(BAR_A_READY(0)); mbar_arrive(BAR_A_READY(1)); }
 
-        const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
+        const int ns = kProgG ? P->n_grad : P->n_fwd;
         float head_part = 0.f;
         for (int s = 0; s < ns; ++s) {
-          const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+          const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
           const int epi = st.epi;
           const bool wa = writes_a(epi);
           for (int h = 0; h < st.nh; ++h) {
@@ -699,7 +716,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
 #pragma unroll
                   for (int e = 0; e < 16; ++e) g[c + e] = __uint_as_float(rg[e]);
                 }
-                if constexpr (Op::kGrad) {
+                if constexpr (kProgG) {
                   if (valid) {
                     if constexpr (Op::kRaw) {
                       op.store_grad_raw(slot, [&](int k) { return (double)g[k]; });
@@ -726,6 +743,9 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                 epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_MASKG_A:
+                if constexpr (Op::kFused)
+                  epi_half<E_MASKG_HEAD_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                else
                 epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_BWD_MASK_A:
@@ -743,19 +763,24 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
               if (lane == 0) mbar_arrive(BAR_A_READY(h));
             }
           }
-          if (epi == E_HEAD) {
+          if (epi == E_HEAD || (Op::kFused && epi == E_MASKG_A)) {
             S.red[sub * ROWS + r] = head_part;
             named_sync(1, N_EPI_WARPS * 32);
             if (sub == 0) {
               double p = (double)(S.red[r] + S.red[ROWS + r] + P->head_b);
               if (F.composite) p = dmul(net.scale, p);
               if (j == j0 || p < best) { best = p; bobj = j; }
+              // fused: the row op sees the distance before the backward's
+              // E_BWD_OUT (same thread) decides whether to keep the gradient
+              if constexpr (Op::kFused) {
+                if (valid) op.store_fwd(slot, best, bobj);
+              }
             }
             named_sync(1, N_EPI_WARPS * 32);
           }
         }
       }
-      if constexpr (!Op::kGrad) {
+      if constexpr (!Op::kGrad && !Op::kFused) {
         if (sub == 0 && valid) op.store_fwd(slot, best, bobj);
       }
     }
@@ -857,6 +882,7 @@ __device__ __forceinline__ void epi_direct_n(int nm, const Step& st, int c_first
   switch (nm) {
     case 1: epi_direct<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
     case 2: epi_direct<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    case 3: epi_direct<EPI, 3>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
     case 4: epi_direct<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
     default: break;
   }
@@ -1657,6 +1683,10 @@ int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op,
   // ping-pong engine below (a two-slot group-per-slot variant measured slower:
   // 880 vs 1065 TF/s forward on 5->8x256, c5 60.1 M vs 69.6 M path samples/s).
   // dbg 512 forces the ping-pong engine (A/B timing).
+  if constexpr (Op::kFused) {
+    // fused trace+gradient exists for the > 256-wide single-tile engine only
+    if (all_pp || F.n_obj != 1) { *err = "fused trace+gradient needs one network wider than 256"; return 1; }
+  } else {
   if (all_pp && maxh <= 128 && !(dbgq & 512))
     return launch_quad<Op, 4>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
   bool pp = true, any_pp = false;
@@ -1666,6 +1696,7 @@ int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op,
   }
   if (any_pp && !pp) { *err = "bf16 engine: networks of one field must all be <= 256 or all > 256 wide"; return 1; }
   if (pp) return launch_pp<Op>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
+  }
   int kmax = 0, chunk = 0, params_bytes = 0;
   for (int j = 0; j < F.n_obj; ++j) {
     kmax = std::max(kmax, images[j].host.kmax);

@@ -28,6 +28,8 @@ struct PathState {
   int* obj;
   double* u34;                     // (P,2) encoded angles of d (neural.py:36-37), set at ray creation
   double* g3;                      // (P,3) spatial input gradient from the gradient pass
+  uint8_t* gdone;                  // 1: g3 already holds this segment's normal gradient (TraceGradOp)
+  uint8_t* want;                   // 1: this segment's normal will be needed and may come from its first march step
 };
 
 struct WaveDev {
@@ -51,6 +53,7 @@ __device__ __forceinline__ void slot_sp(const WaveDev& w, int p, int& s, int& i)
 
 // slab test + march initialisation for a new ray (field.py:265-269)
 __device__ __forceinline__ void begin_trace(const FieldDev& F, const PathState& S, int p, d3 o, d3 d) {
+  if (S.gdone) S.gdone[p] = 0;
   if (F.is_mesh) {   // mesh fields trace every ray exactly (field.py:161-168), no domain box
     S.march[p] = 1;
     S.t[p] = INFINITY;
@@ -173,14 +176,18 @@ __global__ void after_primary_kernel(const WaveDev w, const PathState S, int P) 
 
 // EXTENSION (config 4): Russian roulette at bounce b >= rr_start,
 // survival p = min(1, throughput), survivors divide by p.
+__device__ __forceinline__ bool rr_survives(const WaveDev& w, double thr, int s, int i, int b, double& q) {
+  q = fmin(1.0, thr);
+  const double u = pcg_single(*w.rr, (uint64_t)(s * w.bounces + b) * (uint64_t)w.n_pix + (uint64_t)i);
+  return u < q;
+}
 __global__ void roulette_kernel(const WaveDev w, const PathState S, int P, int b) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P || !S.alive[p]) return;
   int s, i;
   slot_sp(w, p, s, i);
-  const double q = fmin(1.0, S.thr[p]);
-  const double u = pcg_single(*w.rr, (uint64_t)(s * w.bounces + b) * (uint64_t)w.n_pix + (uint64_t)i);
-  if (u < q) S.thr[p] = ddiv(S.thr[p], q);
+  double q;
+  if (rr_survives(w, S.thr[p], s, i, b, q)) S.thr[p] = ddiv(S.thr[p], q);
   else S.alive[p] = 0;
 }
 
@@ -228,6 +235,27 @@ struct GradOutOp : ListBase {
   __device__ void store_grad_raw(int, G) const {}
 };
 
+// Fused normal reuse: march step 0 of a bounce ray evaluates
+// the network at o + t_acc d.  The next bounce's normal (field.py:305-309)
+// evaluates it at o + max(t - delta/2, 0) d with the same angle inputs, so
+// when the two f64 offsets are equal the inputs are identical bit for bit and
+// one kernel can run the forward (distance, hit test, advance) and the
+// backward chain on the same tile: the gradient is kept for exactly those
+// rows (gdone = 1) and the gradient pass of the next bounce skips them.  The
+// result equals the unfused path's: same program, same inputs, same order.
+struct TraceGradOp : TraceStepOp {
+  static constexpr bool kFused = true;
+  double backoff; double* g3; uint8_t* gdone;
+  __device__ void store_grad(int s, const double* g5) const {
+    if (!st.hit[s]) return;
+    if (st.t_acc[s] != fmax(dsub(st.t_out[s], backoff), 0.0)) return;
+    st3(g3, s, mk3(g5[0], g5[1], g5[2]));
+    gdone[s] = 1;
+  }
+  template <class G>
+  __device__ void store_grad_raw(int, G) const {}
+};
+
 // normal + render.py:_hit_normals (127-141) + hit point, throughput, cosine
 // bounce (render.py:226-231) + slab test of the new ray
 __global__ void bounce_kernel(const FieldDev* F, const WaveDev w, const PathState S, const int* list,
@@ -261,6 +289,18 @@ __global__ void bounce_kernel(const FieldDev* F, const WaveDev w, const PathStat
     st3(S.o, p, hp);
     st3(S.d, p, nd);
     begin_trace(*F, S, p, hp, nd);
+    if (S.want) {
+      // fused normal reuse: the next bounce needs this segment's normal only
+      // if there is a next bounce and the path survives its roulette (same
+      // draw and throughput roulette_kernel will see); the first march input
+      // can equal the normal input only for t_acc == 0
+      bool want = b + 1 < w.bounces && S.march[p] && S.t_acc[p] == 0.0;
+      if (want && w.rr_start >= 0 && b + 1 >= w.rr_start) {
+        double q;
+        want = rr_survives(w, S.thr[p], s, i, b + 1, q);
+      }
+      S.want[p] = want;
+    }
   }
 }
 

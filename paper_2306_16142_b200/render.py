@@ -87,6 +87,7 @@ class RenderConfig:
     max_wave_paths: int = 0
     profile: int = 0            # 1: per-kernel-class CUDA-event timing in the stats
     graph: int = 1              # 1: replay the waves as a captured CUDA graph (same camera/config/accumulator)
+    no_fuse: int = 0            # 1: never fuse a bounce's first march step with the next normal (same results)
 
     def __post_init__(self):
         if self.spp < 1:
@@ -135,6 +136,7 @@ def path_struct(config) -> _lib.PathConfig_t:
     p.max_wave_paths = int(getattr(config, "max_wave_paths", 0))
     p.profile = int(getattr(config, "profile", 0))
     p.graph = int(getattr(config, "graph", 1))
+    p.no_fuse = int(getattr(config, "no_fuse", 0))
     return p
 
 

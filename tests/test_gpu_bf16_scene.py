@@ -73,7 +73,8 @@ def bf16_emulation(m, x):
 
 
 @pytest.mark.parametrize("widths", [(5, 128, 128, 128, 128, 1), (5,) + (256,) * 8 + (1,), (65,) + (512,) * 8 + (1,),
-                                    (65,) + (256,) * 6 + (1,), (5, 64, 64, 1), (65, 100, 200, 1), (65, 128, 256, 1)])
+                                    (65,) + (256,) * 6 + (1,), (5, 64, 64, 1), (65, 100, 200, 1), (65, 128, 256, 1),
+                                    (5, 192, 192, 1), (65, 384, 384, 1), (5, 320, 448, 1)])
 def test_bf16_forward_and_gradient(widths):
     m = kaiming_uniform(widths, 3)
     f = CudaNeuralField(m, D, bounds=BOX, precision="bf16")
