@@ -17,7 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libddf_b200.so")
+# DDF_B200_LIB: load another build of the same library (A/B timing)
+LIB_PATH = os.environ.get("DDF_B200_LIB") or os.path.join(LIB_DIR, "libddf_b200.so")
 HEADER = os.path.join(ROOT, "include", "ddf_b200.h")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

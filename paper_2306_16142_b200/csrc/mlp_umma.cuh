@@ -166,6 +166,44 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
+// One 64-wide K chunk (four K = 16 MMAs) in a single asm block, optionally
+// followed by a commit.  The issuing thread is lane 0 of a divergent warp, so
+// every asm block with tcgen05 operands costs an ELECT / R2UR.BROADCAST
+// waterfall; one block per chunk instead of one per MMA (plus per-MMA
+// descriptor rebuilds) cut the issuer's instruction stream ~4x -- it, not
+// the tensor pipe, paced the 512-wide engine (ncu source page: ~90 issue
+// cycles per 128-cycle MMA).  Descriptors advance by 32 B (2 in the >> 4
+// address field) per K step.
+__device__ __forceinline__ void mma_k64(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, %3, %3;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_k64_commit(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t id, uint32_t acc,
+                                               uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, %3, %3;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(id), "r"(acc), "r"(bar)
+      : "memory");
+}
+
 #define DDF_TMEM_LD32(taddr, r)                                                                                   \
   asm volatile(                                                                                                   \
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
@@ -562,6 +600,8 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ar[2] = {0u, 0u};
+      const uint64_t da0 = sdesc(a_base), db0 = sdesc(st_base);
+      const uint32_t sstep = (uint32_t)sstride >> 4;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         int j0, j1, base, nv;
         tile_rows(F, op, t, j0, j1, base, nv);
@@ -599,15 +639,18 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                 tc_after_sync();
                 const long long t_is = kStats ? clock64() : 0;
                 const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
-                const uint32_t a_chunk = a_base + (uint32_t)(kc * ROWS * 128);
-                const uint32_t b_chunk = st_base + (uint32_t)(stage * sstride);
-                if (!(dbg & 128)) {   // dbg 128: timing experiment only, no MMAs (wrong results)
-                  for (int ks = 0; ks < nks; ++ks) {
-                    mma_bf16(tmem + (uint32_t)(h * st.rows), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
-                             (kc | ks) ? 1u : 0u);
-                  }
+                const uint64_t da = da0 + (uint64_t)(kc * (ROWS * 128 / 16));
+                const uint64_t db = db0 + (uint64_t)(stage * sstep);
+                const uint32_t td = tmem + (uint32_t)(h * st.rows);
+                if (kStats && (dbg & 128)) {   // dbg 128: timing experiment only, no MMAs (wrong results)
+                  tc_commit(BAR_EMPTY(stage));
+                } else if (nks == 4) {
+                  mma_k64_commit(td, da, db, id, kc ? 1u : 0u, BAR_EMPTY(stage));
+                } else {
+                  for (int ks = 0; ks < nks; ++ks)
+                    mma_bf16(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
+                  tc_commit(BAR_EMPTY(stage));
                 }
-                tc_commit(BAR_EMPTY(stage));
                 if (wa && h == st.nh - 1) {
                   if (kc == c0) tc_commit(BAR_A_FREE(0));
                   if (kc == st.nchunk - 1) tc_commit(BAR_A_FREE(1));
@@ -1001,6 +1044,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ar[2] = {0u, 0u};
+      const uint64_t db0 = sdesc(st_base);
       for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
         int j0, j1, base, nv;
         pp_rows(F, op, pr, 0, j0, j1, base, nv);
@@ -1019,12 +1063,15 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
                 mbar_wait(BAR_FULL(stage), phase);
                 tc_after_sync();
                 const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
-                const uint32_t a_chunk = a_slot + (uint32_t)(kc * ROWS * 128);
-                const uint32_t b_chunk = st_base + (uint32_t)(stage * stage_bytes);
-                for (int ks = 0; ks < nks; ++ks)
-                  mma_bf16(tmem + (uint32_t)(sl * 256), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
-                           (kc | ks) ? 1u : 0u);
-                tc_commit(BAR_EMPTY(stage));
+                const uint64_t da = sdesc(a_slot) + (uint64_t)(kc * (ROWS * 128 / 16));
+                const uint64_t db = db0 + (uint64_t)(stage * (stage_bytes >> 4));
+                const uint32_t td = tmem + (uint32_t)(sl * 256);
+                if (nks == 4) {
+                  mma_k64_commit(td, da, db, id, kc ? 1u : 0u, BAR_EMPTY(stage));
+                } else {
+                  for (int ks = 0; ks < nks; ++ks) mma_bf16(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
+                  tc_commit(BAR_EMPTY(stage));
+                }
                 if (++stage == n_stages) { stage = 0; phase ^= 1u; }
               }
               tc_commit(BAR_ACC(sl));
@@ -1315,11 +1362,16 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
                   ++ar[sl];
                   tc_after_sync();
                 }
-                const uint32_t a_chunk = a_base0 + (uint32_t)(sl * a_bytes) + (uint32_t)(kc * ROWS * 128);
-                for (int ks = 0; ks < nks; ++ks)
-                  mma_bf16(tmem + (uint32_t)(sl * (512 / NSL)), sdesc(a_chunk + ks * 32), sdesc(b_chunk + ks * 32), id,
-                           (kc | ks) ? 1u : 0u);
-                if (kc == st.nchunk - 1) tc_commit(BAR_ACC(sl));
+                const uint64_t da = sdesc(a_base0 + (uint32_t)(sl * a_bytes)) + (uint64_t)(kc * (ROWS * 128 / 16));
+                const uint64_t db = sdesc(b_chunk);
+                const uint32_t td = tmem + (uint32_t)(sl * (512 / NSL));
+                if (nks == 4) {
+                  if (kc == st.nchunk - 1) mma_k64_commit(td, da, db, id, kc ? 1u : 0u, BAR_ACC(sl));
+                  else mma_k64(td, da, db, id, kc ? 1u : 0u);
+                } else {
+                  for (int ks = 0; ks < nks; ++ks) mma_bf16(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
+                  if (kc == st.nchunk - 1) tc_commit(BAR_ACC(sl));
+                }
               }
               tc_commit(BAR_EMPTY(stage));
               if (++stage == n_stages) { stage = 0; phase ^= 1u; }

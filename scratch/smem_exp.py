@@ -23,3 +23,16 @@ def t(fn, reps=5):
 tf = t(lambda: L.ddf_mlp_forward(f.handle, 0, ctypes.c_void_p(x.data_ptr()), n, ctypes.c_void_p(y.data_ptr()), s))
 tg = t(lambda: L.ddf_mlp_input_grad(f.handle, 0, ctypes.c_void_p(x.data_ptr()), n, ctypes.c_void_p(g.data_ptr()), s))
 print(f"{str(widths[:3]):16s} n={n} dbg={os.environ.get('DDF_DEBUG_UMMA','0')}: fwd {tf:.2f} ms {F*n/tf/1e9:.0f} TF/s | grad {tg:.2f} ms {2*F*n/tg/1e9:.0f} TF/s", flush=True)
+if os.environ.get("STATS"):
+    buf = (ctypes.c_uint64 * 16)()
+    L.ddf_debug_counters(buf, 1)
+    L.ddf_mlp_forward(f.handle, 0, ctypes.c_void_p(x.data_ptr()), n, ctypes.c_void_p(y.data_ptr()), s); torch.cuda.synchronize()
+    L.ddf_debug_counters(buf, 1)
+    c = list(buf)
+    names = ["mma_wait_a_ready", "mma_wait_w_full", "epi_wait_acc(w2)", "epi_wait_a_free(w2)", "mma_total", "mma_steps", "prod_wait_empty", "epi_busy(w2)", "mma_issue"]
+    tiles = (n + 127) // 128
+    per_sm_steps = c[5] / 148
+    print("  forward counters, cycles per (SM x step):", flush=True)
+    for i, nm in enumerate(names):
+        if i == 5: continue
+        print(f"    {nm:22s} {c[i] / max(c[5],1):10.0f}")
