@@ -241,6 +241,11 @@ __device__ __forceinline__ uint32_t a_off(int r, int col) {
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // One epilogue half for one warp: its NM 32-column chunks of the accumulator
@@ -268,17 +273,19 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
       st_shared_v4(blk + (uint32_t)(((cc0 + e) ^ r7) << 4), pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
   };
   // chunk i's epilogue once its accumulator registers are loaded
-  auto proc = [&](const int i, const int c, const uint32_t (&rg)[32]) {
-      // this chunk's operands load while the TMEM read is in flight
-      float4 bq[8];
-      uint32_t mq = 0u;
-      if constexpr (BIAS) {
+  // biases and head weights live in shared memory: explicit ld.shared (short
+  // scoreboard) rather than generic loads, issued before the TMEM wait
+  const uint32_t bias_s = smem_u32(sparams) + 4u * (uint32_t)(size_t)st.bias;
+  const uint32_t head_s = smem_u32(head_w);
+  auto load_bias = [&](int c, float4 (&bq)[8]) {
+    if constexpr (BIAS) {
   #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          bq[k] = *reinterpret_cast<const float4*>(sparams + (size_t)st.bias + c + 4 * k);   // shared memory
-      } else {
-        mq = mpre[i];   // prefetched before the accumulator wait
-      }
+      for (int k = 0; k < 8; ++k) bq[k] = ld_shared_f4(bias_s + 4u * (uint32_t)(c + 4 * k));
+    }
+  };
+  auto proc = [&](const int i, const int c, const uint32_t (&rg)[32], const float4 (&bq)[8]) {
+      uint32_t mq = 0u;
+      if constexpr (!BIAS) mq = mpre[i];   // prefetched before the accumulator wait
       const float* bf = reinterpret_cast<const float*>(bq);
       uint32_t pkd[16];
       if constexpr (EPI == E_BWD_MASK_A) {
@@ -293,7 +300,7 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
       } else if constexpr (EPI == E_HEAD) {
   #pragma unroll
         for (int e = 0; e < 32; e += 4) {
-          const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+          const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
           head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
           head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
           head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
@@ -314,7 +321,7 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
         } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
   #pragma unroll
           for (int e = 0; e < 32; e += 4) {
-            const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+            const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
             if constexpr (EPI == E_MASKG_HEAD_A) {
               // the identity head of the forward, in E_HEAD's order (same fp32 result)
               head_part = fmaf(v[e], hw.x, head_part);
@@ -347,16 +354,23 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
       }
   
   };
-  // TMEM loads are issued two chunks at a time: tcgen05.wait::ld waits for all
-  // outstanding loads, so pairing halves the exposed TMEM round trips
-#pragma unroll
-  for (int i = 0; i < NM; i += 2) {
-    uint32_t rgA[32], rgB[32];
-    DDF_TMEM_LD32(tmem_row + (uint32_t)(c_first + i * 64), rgA);
-    if (i + 1 < NM) DDF_TMEM_LD32(tmem_row + (uint32_t)(c_first + (i + 1) * 64), rgB);
+  // TMEM loads are software-pipelined one chunk ahead: chunk i + 1's load is
+  // in flight while chunk i is processed (8 warps share the SM's TMEM read
+  // port, so the next read overlaps this chunk's math and stores instead of
+  // alternating with them).  tcgen05.wait::ld waits for every outstanding
+  // load, hence one chunk of look-ahead.
+  uint32_t rg[2][32];
+  if constexpr (NM > 0) {
+    DDF_TMEM_LD32(tmem_row + (uint32_t)c_first, rg[0]);
     tmem_wait_ld();
-    proc(i, c_first + i * 64, rgA);
-    if (i + 1 < NM) proc(i + 1, c_first + (i + 1) * 64, rgB);
+  }
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    if (i + 1 < NM) DDF_TMEM_LD32(tmem_row + (uint32_t)(c_first + (i + 1) * 64), rg[(i + 1) & 1]);
+    float4 bq[8];
+    load_bias(c_first + i * 64, bq);
+    proc(i, c_first + i * 64, rg[i & 1], bq);
+    if (i + 1 < NM) tmem_wait_ld();
   }
   if constexpr (WA && NM == 0) ++free_ph;   // no columns in this half: keep the phase count in step
 }
