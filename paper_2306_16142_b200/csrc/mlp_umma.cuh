@@ -690,26 +690,43 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
     const uint32_t a_row = a_base + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);   // this row in every A k-block
     uint32_t* my_masks = mask_scratch + (size_t)blockIdx.x * MASK_WORDS_PER_CTA;
     uint32_t acc_ph[2] = {0u, 0u}, free_ph[2] = {0u, 0u};
+    int staged_j = -1;   // network whose params are in shared memory
+    // this row of the next tile: list entry and path state fetched one tile
+    // ahead (issued once the current tile's encoding is stored, so the two
+    // dependent global round trips overlap the first layer's MMAs instead of
+    // sitting between tiles with the tensor pipe idle)
+    int n_slot = 0;
+    double n_pos[3] = {0.0, 0.0, 0.0}, n_az = 0.0, n_pol = 0.0;
+    auto fetch = [&](int tt) {
+      if (tt < tiles) {
+        int a0, a1, b0, c0;
+        tile_rows(F, op, tt, a0, a1, b0, c0);
+        if (r < c0) {
+          n_slot = op.slot(b0 + r);
+          if constexpr (!Op::kRaw) op.load(n_slot, n_pos, n_az, n_pol);
+        }
+      }
+    };
+    fetch(blockIdx.x);
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int j0, j1, base, nv;
       tile_rows(F, op, t, j0, j1, base, nv);
       const bool valid = r < nv;
-      int slot = 0;
-      double pos[3] = {0.0, 0.0, 0.0}, az = 0.0, pol = 0.0;
-      if (valid) {
-        slot = op.slot(base + r);
-        if constexpr (!Op::kRaw) op.load(slot, pos, az, pol);
-      }
+      const int slot = valid ? n_slot : 0;
+      double pos[3] = {n_pos[0], n_pos[1], n_pos[2]}, az = n_az, pol = n_pol;
       double best = 0.0;
       int bobj = 0;
       for (int j = j0; j < j1; ++j) {
         const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
         const NetDev& net = F.net[j];
-        // this network's biases + head weights -> shared memory (every epilogue
-        // warp is past the previous network's last use: HEAD ends in a named
-        // barrier, gradient programs end with BWD_OUT which reads none)
+        // this network's biases + head weights -> shared memory, only when the
+        // network changes (a single-network field stages them once per launch;
+        // every epilogue warp is past the previous network's last use: HEAD
+        // ends in a named barrier, gradient programs end with BWD_OUT which
+        // reads none)
         const int head_off = __ldg(&P->head_off);
-        {
+        if (j != staged_j) {
+          staged_j = j;
           const int nf = __ldg(&P->params_floats);
           const float4* src = reinterpret_cast<const float4*>(P->params);
           float4* dst = reinterpret_cast<float4*>(S.params);
@@ -737,6 +754,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
         fence_async_smem();
         __syncwarp();
         if (lane == 0) { mbar_arrive(BAR_A_READY(0)); mbar_arrive(BAR_A_READY(1)); }
+        if (j == j0) fetch(t + gridDim.x);
 
         const int ns = kProgG ? P->n_grad : P->n_fwd;
         float head_part = 0.f;
