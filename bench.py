@@ -820,14 +820,22 @@ def main():
     # DRAM traffic per launch of the dominant kernel from the committed ncu
     # --set full capture of this workload (profiles/), next to the
     # algorithmic path-state bytes of that launch
-    ncu_path = os.path.join(ROOT, "profiles", f"r1_{name}_ncu_v7.json")
-    if os.path.exists(ncu_path):
+    ncu_path = None
+    for ver in ("v11", "v7"):
+        cand = os.path.join(ROOT, "profiles", f"r1_{name}_ncu_{ver}.json")
+        if os.path.exists(cand):
+            ncu_path = cand
+            break
+    if ncu_path:
         try:
-            g = json.load(open(ncu_path))["gradient_launch"]
+            rec = json.load(open(ncu_path))
+            key = "fused_launch" if "fused_launch" in rec else "gradient_launch"
+            g = rec[key]
+            kname = g.get("kernel", "mlp_kernel<GradOutOp>").split("(")[0].replace("void ", "")
             roofline["traffic"] = g["traffic_bytes"]
             roofline["traffic_source"] = ("ncu --set full, one %s launch of %.1f ms (%s): %.0f MB DRAM vs ~%.0f MB "
                                           "algorithmic path state; tensor pipe active %.1f%%" % (
-                                              "mlp_kernel<GradOutOp>", g["duration_ms"], os.path.basename(ncu_path),
+                                              kname, g["duration_ms"], os.path.basename(ncu_path),
                                               g["traffic_bytes"] / 1e6, g["algorithmic_state_bytes_est"] / 1e6,
                                               g["tensor_pipe_active_pct_elapsed"]))
         except Exception:
