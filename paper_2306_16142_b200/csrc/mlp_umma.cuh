@@ -314,10 +314,14 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
         for (int e = 0; e < 32; ++e) {
           const float z = __uint_as_float(rg[e]) + bf[e];
           mw |= (z > 0.f ? 1u : 0u) << e;
-          v[e] = fmaxf(z, 0.f);
+          // E_RELU_MASK_A packs with the relu-rounding convert (exact, see
+          // pack_bf16_relu), so it keeps z and skips the FMNMX
+          v[e] = EPI == E_RELU_MASK_A ? z : fmaxf(z, 0.f);
         }
         if constexpr (EPI == E_RELU_MASK_A) {
           my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
+  #pragma unroll
+          for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16_relu(v[2 * e], v[2 * e + 1]);
         } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
   #pragma unroll
           for (int e = 0; e < 32; e += 4) {
@@ -334,9 +338,9 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
             v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
             v[e + 3] = ((mw >> (e + 3)) & 1u) ? hw.w : 0.f;
           }
-        }
   #pragma unroll
-        for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+          for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+        }
       }
       if constexpr (WA) {
         if (i < HOLD) {
