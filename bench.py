@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16", "fp32_simt"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile-balance", default="pilot", choices=["pilot", "rr"],
+                    help="N>1: tiles to ranks by a measured spp=1 pilot (LPT), or round-robin")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank logic with several ranks on one GPU")
     return ap.parse_args()
@@ -710,6 +712,11 @@ def main():
     fld = C.build_field(name, precision=prec)
     cam = C.camera(name)
     cfg = C.render_config(name, rank=rank, world=world)
+    if world > 1 and args.tile_balance == "pilot":
+        # setup, outside the timed region: rank 0's spp=1 pilot costs every
+        # tile, the LPT table is broadcast (dist.balanced_owners_distributed)
+        from paper_2306_16142_b200.dist import balanced_owners_distributed
+        cfg.tile_owner = balanced_owners_distributed(fld, cam, cfg, world, tile=cfg.tile)
     n_pix = cam.width * cam.height
     accum = torch.empty(n_pix, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
@@ -876,6 +883,8 @@ def main():
             "config": {"workload": name, "W": cam.width, "H": cam.height, "spp": cfg.spp, "bounces": cfg.bounces,
                        "widths": list(models[0].widths), "n_networks": len(models), "precision": prec,
                        "tiles": cfg.tile, "parallelism": f"tiles{world}" if world > 1 else "single",
+                       "tile_assignment": (("pilot-balanced (LPT)" if cfg.tile_owner is not None else "round-robin")
+                                           if world > 1 else None),
                        "l2": "flushed (256 MB write) between timed steps"},
             "ddf_queries_per_s": stp["forward_rows"] / (ms / 1e3),
             "gradient_rows_per_s": stp["gradient_rows"] / (ms / 1e3),

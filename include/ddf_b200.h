@@ -79,6 +79,12 @@ typedef struct {
      normal gradient (0 = fuse where the engine and regime allow; results
      are identical either way) */
   int32_t no_fuse;
+  /* nullable: host array of ceil(W/tile) * ceil(H/tile) ranks, tile k owned
+     by rank tile_owner[k] instead of k % world (the cost-balanced assignment
+     of paper_2306_16142_b200/dist.py); read during the call only.  Which rank
+     renders a pixel never changes its value (draws are addressed by global
+     pixel index) */
+  const int32_t* tile_owner;
 } ddf_path_config_t;
 
 typedef struct {

@@ -70,7 +70,7 @@ class PathConfig_t(ctypes.Structure):
                 ("rr_state", ctypes.c_uint64 * 2), ("rr_inc", ctypes.c_uint64 * 2),
                 ("tile", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32), ("graph", ctypes.c_int32),
-                ("no_fuse", ctypes.c_int32)]
+                ("no_fuse", ctypes.c_int32), ("tile_owner", ctypes.POINTER(ctypes.c_int32))]
 
 
 class ModeConfig_t(ctypes.Structure):

@@ -122,6 +122,7 @@ struct ddf_field_s {
   Buf mesh_nodes, mesh_tris, mesh_tof;
   int udf_ndirs = 0;
   int pix_key[6] = {-1, -1, -1, -1, -1, -1};
+  std::vector<int32_t> pix_owner;        // cfg->tile_owner the cached pixel list was built from
   int pix_n = 0;
 };
 
@@ -814,27 +815,39 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   f->prof.reset(cfg->profile != 0);
   size_t t_begin = f->prof.on ? f->prof.rec(st) : 0;
 
-  // owned pixels, ascending global index (cached per film/sharding)
+  // owned pixels, ascending global index (cached per film/sharding/owner table)
   const int key[6] = {cam->width, cam->height, cfg->tile, cfg->rank, cfg->world, 1};
-  if (std::memcmp(key, f->pix_key, sizeof(key)) != 0) {
+  const int T = cfg->tile;
+  const int ntx = T > 0 ? (cam->width + T - 1) / T : 1;
+  const int nty = T > 0 ? (cam->height + T - 1) / T : 1;
+  std::vector<int32_t> owner;
+  if (cfg->tile_owner && T > 0) {
+    owner.assign(cfg->tile_owner, cfg->tile_owner + (size_t)ntx * nty);
+    for (int32_t r : owner)
+      if (r < 0 || r >= cfg->world) return fail(DDF_EUSAGE, "tile_owner entry out of [0, world)");
+  }
+  if (std::memcmp(key, f->pix_key, sizeof(key)) != 0 || owner != f->pix_owner) {
     std::vector<int> own;
     own.reserve(n_pix / cfg->world + 1);
-    const int T = cfg->tile;
-    const int ntx = T > 0 ? (cam->width + T - 1) / T : 1;
-    for (int64_t i = 0; i < n_pix; ++i) {
-      if (T > 0) {
-        const int px = (int)(i % cam->width), py = (int)(i / cam->width);
-        const int tile_id = (py / T) * ntx + px / T;
-        if (tile_id % cfg->world != cfg->rank) continue;
-      } else if (cfg->world > 1 && (i % cfg->world) != cfg->rank) {
-        continue;
-      }
-      own.push_back((int)i);
+    if (T > 0) {
+      // row-major walk one tile-row segment at a time: ascending global ids,
+      // O(H * ntx) ownership tests (the pilot calls this once per tile)
+      for (int py = 0; py < cam->height; ++py)
+        for (int tx = 0; tx < ntx; ++tx) {
+          const int tile_id = (py / T) * ntx + tx;
+          if ((owner.empty() ? tile_id % cfg->world : owner[tile_id]) != cfg->rank) continue;
+          const int x1 = std::min(cam->width, (tx + 1) * T);
+          for (int px = tx * T; px < x1; ++px) own.push_back(py * cam->width + px);
+        }
+    } else {
+      for (int64_t i = 0; i < n_pix; ++i)
+        if (cfg->world == 1 || (i % cfg->world) == cfg->rank) own.push_back((int)i);
     }
     CUDA_TRY(f->pix.ensure(sizeof(int) * std::max<size_t>(1, own.size())));
     if (!own.empty())
       CUDA_TRY(cudaMemcpy(f->pix.p, own.data(), sizeof(int) * own.size(), cudaMemcpyHostToDevice));
     std::memcpy(f->pix_key, key, sizeof(key));
+    f->pix_owner = owner;
     f->pix_n = (int)own.size();
   }
   const int n_own = f->pix_n;
@@ -1009,8 +1022,10 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     auto put = [&](const void* p, size_t n) { gkey.insert(gkey.end(), (const unsigned char*)p, (const unsigned char*)p + n); };
     put(&gen, sizeof gen);
     put(cam, sizeof(*cam));
+    kc.tile_owner = nullptr;   // the table's contents, not its address, key the graph
     put(&kc, sizeof kc);
     put(&acc, sizeof acc);
+    if (!owner.empty()) put(owner.data(), sizeof(int32_t) * owner.size());
   }
   auto epoch_key = [&]() {
     std::vector<unsigned char> k = gkey;

@@ -88,6 +88,7 @@ class RenderConfig:
     profile: int = 0            # 1: per-kernel-class CUDA-event timing in the stats
     graph: int = 1              # 1: replay the waves as a captured CUDA graph (same camera/config/accumulator)
     no_fuse: int = 0            # 1: never fuse a bounce's first march step with the next normal (same results)
+    tile_owner: object = None   # per-tile rank array (dist.balanced_tile_owners); None = tile k -> rank k % world
 
     def __post_init__(self):
         if self.spp < 1:
@@ -137,6 +138,11 @@ def path_struct(config) -> _lib.PathConfig_t:
     p.profile = int(getattr(config, "profile", 0))
     p.graph = int(getattr(config, "graph", 1))
     p.no_fuse = int(getattr(config, "no_fuse", 0))
+    owner = getattr(config, "tile_owner", None)
+    if owner is not None:
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        p._owner_ref = owner   # the struct borrows it for the duration of the call
+        p.tile_owner = owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     return p
 
 

@@ -32,13 +32,13 @@ def _setup(precision):
     return f, cam, cfg
 
 
-def _worker(rank, world, port, precision, out):
+def _worker(rank, world, port, precision, out, tile_owner=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2306_16142_b200.dist import render_path_distributed
     f, cam, cfg = _setup(precision)
-    fb, stats = render_path_distributed(f, cam, cfg)
+    fb, stats = render_path_distributed(f, cam, cfg, tile_owner=tile_owner)
     out.put((rank, np.asarray(fb.data).tobytes(), int(stats["path_samples"])))
     dist.barrier()
     dist.destroy_process_group()
@@ -50,13 +50,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16"])
-def test_two_rank_render_equals_single_rank(precision):
+@pytest.mark.parametrize("precision,balance", [("fp32", None), ("bf16", None), ("bf16", "balanced")])
+def test_two_rank_render_equals_single_rank(precision, balance):
     from paper_2306_16142_b200 import render as R
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, precision, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, precision, q, balance)) for r in range(2)]
     for p in procs:
         p.start()
     got = [q.get(timeout=600) for _ in procs]
@@ -68,3 +68,37 @@ def test_two_rank_render_equals_single_rank(precision):
     films = {r: np.frombuffer(b, dtype=want.dtype).reshape(want.shape) for r, b, _ in got}
     assert np.array_equal(films[0], want) and np.array_equal(films[1], want)
     assert sum(n for _, _, n in got) == W * H * cfg.spp
+
+
+def test_tile_owner_table_partitions_film_exactly():
+    """Three ranks under a pilot-balanced table (and a hand-made one): the
+    per-rank films are disjoint and sum bit-exactly to the 1-rank film; a bad
+    table entry is a usage error."""
+    import torch as T
+
+    from paper_2306_16142_b200 import render as R
+    from paper_2306_16142_b200.dist import balanced_tile_owners, measure_tile_costs, owned_pixels, tile_config
+    f, cam, cfg = _setup("bf16")
+    want, _ = R.render_path_device(f, cam, R.RenderConfig(**{**cfg.__dict__, "graph": 0}))
+    want = want.cpu().numpy()
+    cost = measure_tile_costs(f, cam, cfg, tile=32)
+    assert cost.shape == (((W + 31) // 32) * ((H + 31) // 32),) and np.all(cost > 0)
+    for owner in (balanced_tile_owners(cost, 3), np.array([2, 2, 2, 2, 2, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1])):
+        total = np.zeros_like(want)
+        for rank in range(3):
+            c = tile_config(cfg, rank, 3, tile=32, tile_owner=owner)
+            c.tile = 32
+            acc, st = R.render_path_device(f, cam, c)
+            acc = acc.cpu().numpy()
+            mine = owned_pixels(W, H, 32, rank, 3, owner)
+            assert st["path_samples"] == len(mine) * cfg.spp
+            other = np.ones(W * H, bool)
+            other[mine] = False
+            assert np.all(acc[other] == 0.0)
+            total += acc
+        assert np.array_equal(total, want)
+    bad = tile_config(cfg, 0, 3, tile=32, tile_owner=np.full(15, 3))
+    bad.tile = 32
+    with pytest.raises(ValueError, match="tile_owner"):
+        R.render_path_device(f, cam, bad)
+    T.cuda.synchronize()
