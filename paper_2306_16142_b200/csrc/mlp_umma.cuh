@@ -278,10 +278,24 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
   const uint32_t bias_s = smem_u32(sparams) + 4u * (uint32_t)(size_t)st.bias;
   const uint32_t head_s = smem_u32(head_w);
   auto load_bias = [&](int c, float4 (&bq)[8]) {
+#ifdef DDF_EXP_NOBIAS
+    if constexpr (false) {
+#else
     if constexpr (BIAS) {
+#endif
   #pragma unroll
       for (int k = 0; k < 8; ++k) bq[k] = ld_shared_f4(bias_s + 4u * (uint32_t)(c + 4 * k));
     }
+  };
+  // z = accumulator + bias.  DDF_EXP_NOBIAS (timing experiment only, exact
+  // only for zero biases) drops the add to measure what it costs
+  auto zb = [](uint32_t acc, float b) {
+#ifdef DDF_EXP_NOBIAS
+    (void)b;
+    return __uint_as_float(acc);
+#else
+    return __uint_as_float(acc) + b;
+#endif
   };
   auto proc = [&](const int i, const int c, const uint32_t (&rg)[32], const float4 (&bq)[8]) {
       uint32_t mq = 0u;
@@ -296,15 +310,15 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
       } else if constexpr (EPI == E_RELU_A) {
   #pragma unroll
         for (int e = 0; e < 16; ++e)
-          pkd[e] = pack_bf16_relu(__uint_as_float(rg[2 * e]) + bf[2 * e], __uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1]);
+          pkd[e] = pack_bf16_relu(zb(rg[2 * e], bf[2 * e]), zb(rg[2 * e + 1], bf[2 * e + 1]));
       } else if constexpr (EPI == E_HEAD) {
   #pragma unroll
         for (int e = 0; e < 32; e += 4) {
           const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
-          head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
-          head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
-          head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
-          head_part = fmaf(fmaxf(__uint_as_float(rg[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+          head_part = fmaf(fmaxf(zb(rg[e], bf[e]), 0.f), hw.x, head_part);
+          head_part = fmaf(fmaxf(zb(rg[e + 1], bf[e + 1]), 0.f), hw.y, head_part);
+          head_part = fmaf(fmaxf(zb(rg[e + 2], bf[e + 2]), 0.f), hw.z, head_part);
+          head_part = fmaf(fmaxf(zb(rg[e + 3], bf[e + 3]), 0.f), hw.w, head_part);
         }
       } else {
         // ReLU mask bits of this row's 32 columns (neural.py:241 "h > 0")
@@ -312,7 +326,7 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
         float v[32];
   #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const float z = __uint_as_float(rg[e]) + bf[e];
+          const float z = zb(rg[e], bf[e]);
           mw |= (z > 0.f ? 1u : 0u) << e;
           // E_RELU_MASK_A packs with the relu-rounding convert (exact, see
           // pack_bf16_relu), so it keeps z and skips the FMNMX
