@@ -154,6 +154,12 @@ def render_path_device(backend, camera, config, accum=None, stream=None):
     n_pix = camera.width * camera.height
     if accum is None:
         accum = torch.empty(n_pix, dtype=torch.float64, device=backend.torch_device)
+    owner = getattr(config, "tile_owner", None)
+    tile = int(getattr(config, "tile", 0))
+    if owner is not None and tile > 0:
+        n_tiles = -(-camera.width // tile) * -(-camera.height // tile)
+        if np.size(owner) != n_tiles:
+            raise ValueError(f"tile_owner has {np.size(owner)} entries, the film has {n_tiles} tiles")
     st = _lib.RenderStats_t()
     cam = camera_struct(camera)
     cfg = path_struct(config)

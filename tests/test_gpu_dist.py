@@ -101,4 +101,8 @@ def test_tile_owner_table_partitions_film_exactly():
     bad.tile = 32
     with pytest.raises(ValueError, match="tile_owner"):
         R.render_path_device(f, cam, bad)
+    short = tile_config(cfg, 0, 3, tile=32, tile_owner=np.zeros(14))
+    short.tile = 32
+    with pytest.raises(ValueError, match="tile_owner has 14"):
+        R.render_path_device(f, cam, short)
     T.cuda.synchronize()
