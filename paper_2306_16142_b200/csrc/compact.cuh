@@ -9,6 +9,10 @@
 //   pass 3  scatter    warp ballot ranks + per-warp prefix -> list
 // HBM traffic: flags (1 B) + obj (4 B, bucketed only) read twice, 4 B written
 // per survivor.
+//
+// Unbucketed lists (one segment) take the single-pass kernel instead:
+// onepass_kernel reads the flags once and finds its block's offset by
+// decoupled look-back over the predecessors' published counts.
 #pragma once
 #include "ddf_common.cuh"
 
@@ -116,6 +120,121 @@ __global__ void __launch_bounds__(NT) scatter_kernel(const uint8_t* __restrict__
       run += total;
       __syncthreads();
     }
+  }
+}
+
+// ---------------------------------------------------------------- single pass
+// state[b] (zeroed before the launch, with the ticket counter at state[nb]):
+// bits 32-33 = 1 aggregate published, 2 inclusive prefix published; bits 0-31
+// the count.  Blocks take tickets in launch order, so every predecessor a
+// block waits on is already resident and never waits on a successor.
+constexpr unsigned long long ST_AGG = 1ull << 32, ST_INC = 2ull << 32;
+
+__device__ __forceinline__ unsigned long long ld_state(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_state(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+constexpr int OP_IPT = 32;                  // contiguous slots per thread
+constexpr int OP_ITEMS = NT * OP_IPT;       // 8192 slots per block: a short look-back chain
+
+__global__ void __launch_bounds__(NT) onepass_kernel(const uint8_t* __restrict__ flags, const uint8_t* __restrict__ sel,
+                                                     int sel_val, int n, int nb, unsigned long long* state,
+                                                     int* __restrict__ list, int* __restrict__ seg,
+                                                     int* __restrict__ count, unsigned long long* rows_acc,
+                                                     unsigned long long* rows_acc2) {
+  __shared__ int warp_tot[NT / 32];
+  __shared__ int s_ticket, s_excl;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_ticket = (int)atomicAdd(&state[nb], 1ull);
+  __syncthreads();
+  const int b = s_ticket;
+  const int base = b * OP_ITEMS + threadIdx.x * OP_IPT;
+  // this thread's 32 slots as a bit mask (vector loads when fully in range)
+  uint32_t bits = 0u;
+  if (base + OP_IPT <= n && (((uintptr_t)(flags + base) | (uintptr_t)(sel ? sel + base : nullptr)) & 15u) == 0) {
+    const uint4* fv = reinterpret_cast<const uint4*>(flags + base);
+    const uint4 f0 = __ldg(fv), f1 = __ldg(fv + 1);
+    const uint32_t fw[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+    uint32_t sw[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (sel) {
+      const uint4* sv = reinterpret_cast<const uint4*>(sel + base);
+      const uint4 s0 = __ldg(sv), s1 = __ldg(sv + 1);
+      sw[0] = s0.x; sw[1] = s0.y; sw[2] = s0.z; sw[3] = s0.w; sw[4] = s1.x; sw[5] = s1.y; sw[6] = s1.z; sw[7] = s1.w;
+    }
+#pragma unroll
+    for (int e = 0; e < OP_IPT; ++e) {
+      const bool fl = ((fw[e >> 2] >> (8 * (e & 3))) & 0xffu) != 0u;
+      const bool sl = !sel || (int)((sw[e >> 2] >> (8 * (e & 3))) & 0xffu) == sel_val;
+      bits |= (fl && sl ? 1u : 0u) << e;
+    }
+  } else {
+    for (int e = 0; e < OP_IPT; ++e) bits |= (take(flags, sel, sel_val, nullptr, base + e, n, 0) ? 1u : 0u) << e;
+  }
+  const int cnt = __popc(bits);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int wt = lane < NT / 32 ? warp_tot[lane] : 0;
+    int agg = wt;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(0xffffffffu, agg, o);
+    if (b == 0) {
+      if (lane == 0) {
+        st_state(&state[0], ST_INC | (unsigned)agg);
+        s_excl = 0;
+      }
+    } else {
+      if (lane == 0) st_state(&state[b], ST_AGG | (unsigned)agg);
+      int excl = 0;
+      int p = b - 1 - lane;   // this lane's predecessor in the current window
+      while (true) {
+        unsigned long long v = ST_INC;   // before block 0: an inclusive prefix of 0
+        if (p >= 0) {
+          do { v = ld_state(&state[p]); } while ((v >> 32) == 0ull);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (v >> 32) == 2ull);
+        // lanes up to and including the nearest inclusive prefix contribute
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        int val = lane <= stop ? (int)(v & 0xffffffffu) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        excl += val;
+        if (inc) break;
+        p -= 32;
+      }
+      if (lane == 0) {
+        st_state(&state[b], ST_INC | (unsigned)(excl + agg));
+        s_excl = excl;
+      }
+    }
+  }
+  __syncthreads();
+  int before = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) before += (w < warp) ? warp_tot[w] : 0;
+  int pos = s_excl + before + incl - cnt;
+  while (bits) {
+    const int e = __ffs(bits) - 1;
+    list[pos++] = base + e;
+    bits &= bits - 1u;
+  }
+  if (b == nb - 1 && threadIdx.x == NT - 1) {   // the last thread of the last block ends at the total
+    seg[0] = 0;
+    seg[1] = pos;
+    *count = pos;
+    if (rows_acc) *rows_acc += (unsigned long long)pos;
+    if (rows_acc2) *rows_acc2 += (unsigned long long)pos;
   }
 }
 

@@ -252,10 +252,20 @@ int compact_flags(ddf_field_s* f, const uint8_t* flags, const int* obj, int n, i
                   int* count, unsigned long long* rows_acc, cudaStream_t st, const uint8_t* sel = nullptr,
                   int sel_val = 0, unsigned long long* rows_acc2 = nullptr) {
   const int nb = std::max(1, (n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS);
-  CUDA_TRY(f->blocks.ensure(sizeof(int) * nb * DDF_MAX_OBJECTS));
+  CUDA_TRY(f->blocks.ensure(std::max(sizeof(int) * nb * DDF_MAX_OBJECTS, sizeof(unsigned long long) * (nb + 1))));
   int* bc = f->blocks.as<int>();
   const int no = obj ? n_obj : 1;
   ProfScope ps(f->prof, Prof::COMPACT, st);
+  if (no == 1) {   // one segment: single pass with decoupled look-back
+    const int nb1 = std::max(1, (n + compact::OP_ITEMS - 1) / compact::OP_ITEMS);
+    unsigned long long* state = f->blocks.as<unsigned long long>();
+    CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb1 + 1), st));
+    f->prof.launches += 1;
+    compact::onepass_kernel<<<nb1, compact::NT, 0, st>>>(flags, sel, sel_val, n, nb1, state, list, seg, count,
+                                                          rows_acc, rows_acc2);
+    CUDA_TRY(cudaGetLastError());
+    return DDF_OK;
+  }
   f->prof.launches += 3;
   compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, sel, sel_val, obj, n, no, bc);
   compact::scan_kernel<<<1, 1024, 0, st>>>(bc, nb, no, seg, count, rows_acc, rows_acc2);
@@ -1222,11 +1232,13 @@ int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, 
   if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad count");
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = std::max<int>(1, (int)((n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS));
-  CUDA_TRY(g_cs.blocks.ensure(sizeof(int) * nb));
+  CUDA_TRY(g_cs.blocks.ensure(sizeof(unsigned long long) * (nb + 1)));
   CUDA_TRY(g_cs.seg.ensure(sizeof(int) * 2));
-  compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, 0, nullptr, (int)n, 1, g_cs.blocks.as<int>());
-  compact::scan_kernel<<<1, 1024, 0, st>>>(g_cs.blocks.as<int>(), nb, 1, g_cs.seg.as<int>(), count, nullptr, nullptr);
-  compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, nullptr, 0, nullptr, (int)n, 1, g_cs.blocks.as<int>(), list);
+  const int nb1 = std::max<int>(1, (int)((n + compact::OP_ITEMS - 1) / compact::OP_ITEMS));
+  unsigned long long* state = g_cs.blocks.as<unsigned long long>();
+  CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb1 + 1), st));
+  compact::onepass_kernel<<<nb1, compact::NT, 0, st>>>(flags, nullptr, 0, (int)n, nb1, state, list,
+                                                        g_cs.seg.as<int>(), count, nullptr, nullptr);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(st));
   return DDF_OK;

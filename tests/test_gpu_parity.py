@@ -123,7 +123,29 @@ def test_rng_bit_exact(golden):
         assert got[64 + j] == O.pcg_double((s, inc), k)
 
 
-@pytest.mark.parametrize("n", [0, 1, 1023, 1024, 1025, 70001])
+def test_compaction_single_pass_large_and_repeated():
+    """The single-pass (decoupled look-back) list over 8 M slots with long
+    all-dead and all-live runs (look-back windows that see only aggregates),
+    called repeatedly on one stream (the block-state reset between calls)."""
+    n = 8_000_001
+    rng = np.random.default_rng(11)
+    for density in (0.5, 0.003, 1.0):
+        flags = (rng.random(n) < density).astype(np.uint8)
+        flags[1_000_000:3_500_000] = 0
+        flags[5_000_000:5_600_000] = 1
+        fd = torch.from_numpy(flags).cuda()
+        ref = np.nonzero(flags)[0]
+        for _ in range(2):
+            lst = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+            cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+            _lib.check(_lib.lib().ddf_compact(ctypes.c_void_p(fd.data_ptr()), n, ctypes.c_void_p(lst.data_ptr()),
+                                              ctypes.c_void_p(cnt.data_ptr()), None))
+            c = int(cnt.item())
+            assert c == len(ref)
+            assert np.array_equal(lst[:c].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 1023, 1024, 1025, 32 * 1024 + 1, 70001])
 def test_compaction_bit_exact(n):
     rng = np.random.default_rng(n)
     flags = (rng.random(n) < 0.37).astype(np.uint8)
