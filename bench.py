@@ -353,8 +353,8 @@ def bench_udf(args, rank, world, local):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("bf16_tflops", 1590.0))
     n_scan = -(-n // ((1 << 25) // UDF_DIRS))
-    # grid points, scan + argmin per chunk, compaction (3) + count, init, 4 x (begin, 13 probes, 12 steps, end), scatter
-    launches = 1 + 2 * n_scan + 3 + 1 + 1 + 4 * 27 + 1
+    # grid points, scan + argmin per chunk, compaction (1, single pass) + count, init, 4 x (begin, 13 probes, 12 steps, end), scatter
+    launches = 1 + 2 * n_scan + 1 + 1 + 1 + 4 * 27 + 1
     res = {"metric": "udf_points_per_s", "value": n / (ms / 1e3), "unit": "udf_points/s", "n_gpus": world,
            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
@@ -808,15 +808,17 @@ def main():
                             "inputs coincide (SURVEY 8(d) fused normal reuse): forward F + backward F per row"},
                 "compaction_ms": stp["ms_compact"], "other_ms": stp["ms_other"], "profiled_step_ms": stp["ms_total"]}
     # wavefront compaction against HBM: per compaction call the
-    # flags are read twice (plus 4 B object ids twice when bucketed) and 4 B
-    # are written per survivor; the survivors are exactly the MLP rows
+    # flags are read once (single pass), or twice with the 4 B object ids when
+    # bucketed (the scene's bounce stage), and 4 B are written per survivor;
+    # the survivors are exactly the MLP rows
     import math
     lo_b, hi_b = np.asarray(C.SCENE_BOX if w.get("scene") else C.UNIT_BOX)
     diag = float(np.sqrt(((hi_b - lo_b) ** 2).sum()))
     max_steps = math.ceil(diag / (0.9 * C.delta(name))) + 4
     samples = int(stp["path_samples"])
     calls = max_steps * (1 + cfg.bounces) + cfg.bounces
-    cbytes = 2 * samples * calls + (8 * samples * cfg.bounces if w.get("scene") else 0) \
+    bucketed = cfg.bounces if w.get("scene") else 0
+    cbytes = samples * (calls - bucketed) + (2 + 8) * samples * bucketed \
         + 4 * (stp["forward_rows"] + stp["gradient_rows"])
     hbm = float(peaks.get("hbm_gbs", 6540.5))
     if stp["ms_compact"]:
