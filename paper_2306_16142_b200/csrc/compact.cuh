@@ -7,8 +7,8 @@
 //   pass 2  scan       one CTA: exclusive scan of block counts -> offsets,
 //                      segment table seg[0..n_obj], total -> *count
 //   pass 3  scatter    warp ballot ranks + per-warp prefix -> list
-// HBM traffic: flags (1 B) + obj (4 B, bucketed only) read twice, 4 B written
-// per survivor.
+// HBM traffic: flags (1 B) + obj (4 B, bucketed only) read twice (once per
+// pass, whatever the object count), 4 B written per survivor.
 //
 // Unbucketed lists (one segment) take the single-pass kernel instead:
 // onepass_kernel reads the flags once and finds its block's offset by
@@ -37,13 +37,18 @@ __global__ void __launch_bounds__(NT) count_kernel(const uint8_t* __restrict__ f
   __syncthreads();
   const int base = blockIdx.x * BLOCK_ITEMS;
   const int lane = threadIdx.x & 31;
+  // each slot's flag and object id are read once; the per-object ballots
+  // below work on registers (-1 = not taken)
+  int oid[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int idx = base + i * NT + threadIdx.x;
+    oid[i] = take(flags, sel, sel_val, nullptr, idx, n, 0) ? (obj ? obj[idx] : 0) : -1;
+  }
   for (int j = 0; j < n_obj; ++j) {
     int c = 0;
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const unsigned b = __ballot_sync(0xffffffffu, take(flags, sel, sel_val, obj, base + i * NT + threadIdx.x, n, j));
-      c += __popc(b);
-    }
+    for (int i = 0; i < IPT; ++i) c += __popc(__ballot_sync(0xffffffffu, oid[i] == j));
     if (lane == 0 && c) atomicAdd(&cnt[j], c);
   }
   __syncthreads();
@@ -101,11 +106,18 @@ __global__ void __launch_bounds__(NT) scatter_kernel(const uint8_t* __restrict__
   const int base = blockIdx.x * BLOCK_ITEMS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  int oid[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int idx = base + i * NT + threadIdx.x;
+    oid[i] = take(flags, sel, sel_val, nullptr, idx, n, 0) ? (obj ? obj[idx] : 0) : -1;
+  }
   for (int j = 0; j < n_obj; ++j) {
     int run = block_offsets[blockIdx.x * n_obj + j];
+#pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const int idx = base + i * NT + threadIdx.x;
-      const bool t = take(flags, sel, sel_val, obj, idx, n, j);
+      const bool t = oid[i] == j;
       const unsigned b = __ballot_sync(0xffffffffu, t);
       if (lane == 0) warp_cnt[warp] = __popc(b);
       __syncthreads();
