@@ -6,7 +6,7 @@
 //   pass 1  count      per 1024-slot block, per object (warp ballot + popc)
 //   pass 2  scan       one CTA: exclusive scan of block counts -> offsets,
 //                      segment table seg[0..n_obj], total -> *count
-//   pass 3  scatter    warp ballot ranks + per-warp prefix -> list
+//   pass 3  scatter    match-any ranks per object + per-warp prefix -> list
 // HBM traffic: flags (1 B) + obj (4 B, bucketed only) read twice (once per
 // pass, whatever the object count), 4 B written per survivor.
 //
@@ -102,36 +102,38 @@ __global__ void __launch_bounds__(NT) scatter_kernel(const uint8_t* __restrict__
                                                      int sel_val, const int* __restrict__ obj,
                                                      int n, int n_obj, const int* __restrict__ block_offsets,
                                                      int* __restrict__ list) {
-  __shared__ int warp_cnt[NT / 32];
+  // one pass over the block for every object: __match_any_sync groups a
+  // warp's lanes by object id; wc[i][w][j] = slots of object j in warp w's
+  // i-th 32-slot row.  A slot's position is its object's block offset plus
+  // the same-object slots before it in index order (i, warp, lane).
+  __shared__ int wc[IPT][NT / 32][DDF_MAX_OBJECTS];
   const int base = blockIdx.x * BLOCK_ITEMS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  for (int k = threadIdx.x; k < IPT * (NT / 32) * DDF_MAX_OBJECTS; k += NT) (&wc[0][0][0])[k] = 0;
+  __syncthreads();
   int oid[IPT];
+  unsigned grp[IPT];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int idx = base + i * NT + threadIdx.x;
-    oid[i] = take(flags, sel, sel_val, nullptr, idx, n, 0) ? (obj ? obj[idx] : 0) : -1;
+    int o = take(flags, sel, sel_val, nullptr, idx, n, 0) ? (obj ? obj[idx] : 0) : -1;
+    if (o >= n_obj) o = -1;   // ids outside [0, n_obj) are never listed
+    oid[i] = o;
+    grp[i] = __match_any_sync(0xffffffffu, o);
+    if (o >= 0 && (grp[i] & lt) == 0u) wc[i][warp][o] = __popc(grp[i]);
   }
-  for (int j = 0; j < n_obj; ++j) {
-    int run = block_offsets[blockIdx.x * n_obj + j];
+  __syncthreads();
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const int idx = base + i * NT + threadIdx.x;
-      const bool t = oid[i] == j;
-      const unsigned b = __ballot_sync(0xffffffffu, t);
-      if (lane == 0) warp_cnt[warp] = __popc(b);
-      __syncthreads();
-      int before = 0, total = 0;
+  for (int i = 0; i < IPT; ++i) {
+    const int j = oid[i];
+    if (j < 0) continue;
+    int pos = block_offsets[blockIdx.x * n_obj + j] + __popc(grp[i] & lt);
 #pragma unroll
-      for (int w = 0; w < NT / 32; ++w) {
-        const int c = warp_cnt[w];
-        before += (w < warp) ? c : 0;
-        total += c;
-      }
-      if (t) list[run + before + __popc(b & lt)] = idx;
-      run += total;
-      __syncthreads();
-    }
+    for (int i2 = 0; i2 < IPT; ++i2)
+#pragma unroll
+      for (int w = 0; w < NT / 32; ++w) pos += (i2 < i || (i2 == i && w < warp)) ? wc[i2][w][j] : 0;
+    list[pos] = base + i * NT + threadIdx.x;
   }
 }
 
