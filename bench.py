@@ -213,10 +213,12 @@ def bench_queries(args, rank, world, local):
             times.append(e0.elapsed_time(e1))
         clk.top_up(step)
     ms = float(np.mean(times))
-    # e2e through the public protocol call (numpy in, numpy out)
-    f.query_raw(o, d)
+    # e2e through the public protocol call (numpy in, numpy out); the call
+    # takes well under a millisecond, so the mean is over at least 20 calls
+    for _ in range(3):
+        f.query_raw(o, d)
     te = []
-    for _ in range(args.steps):
+    for _ in range(max(args.steps, 20)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         f.query_raw(o, d)

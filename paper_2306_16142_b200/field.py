@@ -35,6 +35,20 @@ def _dev(a, dtype=torch.float64, device="cuda"):
     return t.to(device, non_blocking=True)
 
 
+def _host(*ts):
+    """Device tensors -> numpy through pinned buffers: asynchronous copies on
+    the current stream and one synchronize (a pageable .cpu() per output pays
+    a staged copy and a sync each).  The arrays view their pinned tensors,
+    which they keep alive."""
+    outs = []
+    for t in ts:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in outs]
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
@@ -118,7 +132,8 @@ class CudaNeuralField:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and _lib._lib is not None:
+        # at interpreter exit the module globals may already be gone
+        if h is not None and _lib is not None and getattr(_lib, "_lib", None) is not None:
             _lib._lib.ddf_field_destroy(h)
             self._h = None
 
@@ -145,7 +160,7 @@ class CudaNeuralField:
         xd = _dev(x, device=self.torch_device)
         out = torch.empty(len(x), dtype=torch.float64, device=self.torch_device)
         _lib.check(_lib.lib().ddf_mlp_forward(self._h, net, _ptr(xd), len(x), _ptr(out), _stream()))
-        return out.cpu().numpy()
+        return _host(out)[0]
 
     def input_gradient_inputs(self, inputs, net: int = 0):
         """neural.input_gradient_batch (neural.py:229-249) on raw inputs."""
@@ -153,7 +168,7 @@ class CudaNeuralField:
         xd = _dev(x, device=self.torch_device)
         out = torch.empty(x.shape, dtype=torch.float64, device=self.torch_device)
         _lib.check(_lib.lib().ddf_mlp_input_grad(self._h, net, _ptr(xd), len(x), _ptr(out), _stream()))
-        return out.cpu().numpy()
+        return _host(out)[0]
 
     def query_raw(self, positions, dir_vecs):
         """(pred, t, hit, obj): the raw network distance next to query_batch."""
@@ -165,7 +180,8 @@ class CudaNeuralField:
         obj = torch.empty(n, dtype=torch.int32, device=self.torch_device)
         _lib.check(_lib.lib().ddf_query(self._h, _ptr(pd), _ptr(dd), n, _ptr(t), _ptr(hit), _ptr(pred), _ptr(obj),
                                         _stream()))
-        return pred.cpu().numpy(), t.cpu().numpy(), hit.cpu().numpy().astype(bool), obj.cpu().numpy()
+        pred, t, hit, obj = _host(pred, t, hit, obj)
+        return pred, t, hit.astype(bool), obj
 
     def query_batch(self, positions, dir_vecs):
         """field.py:257-258 -> (t, hit)."""
@@ -186,7 +202,8 @@ class CudaNeuralField:
         hit = torch.empty(n, dtype=torch.uint8, device=self.torch_device)
         obj = torch.empty(n, dtype=torch.int32, device=self.torch_device)
         _lib.check(_lib.lib().ddf_trace(self._h, _ptr(od), _ptr(dd), n, _ptr(t), _ptr(hit), _ptr(obj), _stream()))
-        return t.cpu().numpy(), hit.cpu().numpy().astype(bool), obj.cpu().numpy()
+        t, hit, obj = _host(t, hit, obj)
+        return t, hit.astype(bool), obj
 
     def trace_batch(self, origins, dir_vecs):
         """field.py:260-289 -> (t with inf on miss, hit)."""
@@ -203,7 +220,8 @@ class CudaNeuralField:
         valid = torch.empty(n, dtype=torch.uint8, device=self.torch_device)
         _lib.check(_lib.lib().ddf_normal(self._h, _ptr(od), _ptr(dd), _ptr(th), _ptr(ob), n, _ptr(nr), _ptr(valid),
                                          _stream()))
-        return nr.cpu().numpy(), valid.cpu().numpy().astype(bool)
+        nr, valid = _host(nr, valid)
+        return nr, valid.astype(bool)
 
     def input_gradients(self, positions, angles):
         """field.py:291-293: (N, 5) gradient w.r.t. the encoded inputs
