@@ -26,7 +26,9 @@ from .neural import effective_weights, encoding_of, load_model
 
 def _dev(a, dtype=torch.float64, device="cuda"):
     """numpy -> device tensor through pinned memory (the host<->device copy a
-    protocol call pays)."""
+    protocol call pays).  Measured in situ against a direct pageable copy and
+    against one shared pinned buffer for both inputs: both were slower
+    (query_raw 314 us here vs 423 and 418 us; scratch/e2e_ab.py)."""
     t = torch.from_numpy(np.ascontiguousarray(a))
     if dtype is not None:
         t = t.to(dtype)
