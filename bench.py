@@ -375,7 +375,14 @@ def bench_udf(args, rank, world, local):
 
 
 # ----------------------------------------------------------------- BVH mesh render
-BVH_MESH = ("blob", 4, 0)     # meshes.blob(4, 0): 5,120 triangles, the reference's bunny-class test mesh
+BVH_MESH = "blob4"     # the reference's meshes.blob(4, 0): 5,120 triangles (tests/golden/reference_meshes.npz)
+
+
+def reference_mesh(key=BVH_MESH):
+    """(vertices, faces) of one of the reference's procedural meshes, as
+    tests/golden/make_golden.py stored them."""
+    z = np.load(os.path.join(ROOT, "tests", "golden", "reference_meshes.npz"))
+    return z[f"{key}_v"], z[f"{key}_f"]
 
 
 def cpu_bvh(args, reference_line=False):
@@ -383,9 +390,7 @@ def cpu_bvh(args, reference_line=False):
     linear scan (BruteForceField semantics) on a bounded band sample."""
     from oracle import cpu_ddf as O
     from paper_2306_16142_b200 import configs as C
-    from paper_2306_16142_b200 import meshes as MS
-    m = MS.blob(*BVH_MESH[1:])
-    f = O.MeshField(m.vertices, m.faces)
+    f = O.MeshField(*reference_mesh())
     w = C.WORKLOADS["c3"]
     cam = O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=w["W"], height=w["H"])
     cfg = O.PathConfig(spp=1, bounces=w["bounces"], albedo=0.7, env=1.0, seed=C.RENDER_SEED)
@@ -415,13 +420,11 @@ def bench_bvh(args, rank, world, local):
     DDF-vs-BVH render timing (Fig. 5)."""
     import torch
     from paper_2306_16142_b200 import configs as C
-    from paper_2306_16142_b200 import meshes as MS
     from paper_2306_16142_b200 import render as R
     from paper_2306_16142_b200.mesh import CudaMeshField
     dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
-    m = MS.blob(*BVH_MESH[1:])
-    fld = CudaMeshField(m)
+    fld = CudaMeshField(reference_mesh())
     cam = C.camera("c3")
     cfg = C.render_config("c3")
     n_pix = cam.width * cam.height
@@ -504,7 +507,6 @@ def bench_modes(args, rank, world, local):
     the exact BVH mesh (Fig. 5's BVH side).  One step = the three DDF modes."""
     import torch
     from paper_2306_16142_b200 import configs as C
-    from paper_2306_16142_b200 import meshes as MS
     from paper_2306_16142_b200 import render as R
     from paper_2306_16142_b200.mesh import CudaMeshField
     dev = local % max(1, torch.cuda.device_count())
@@ -512,7 +514,7 @@ def bench_modes(args, rank, world, local):
     W, H = 1920, 1080
     prec = args.precision or "bf16"
     f = C.build_field("c4", precision=prec)
-    mesh = CudaMeshField(MS.blob(4, 0))
+    mesh = CudaMeshField(reference_mesh("blob4"))
     cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=W, height=H)
     modes = ("depth", "normal", "shaded")
 

@@ -19,7 +19,8 @@
  *    whenever a handle first sees a new direction count (direction table).
  *  - One call at a time per field handle (its scratch is reused); handles are
  *    independent, so concurrent calls on different handles are fine.
- *    ddf_compact uses process-wide scratch: one caller thread at a time.
+ *    ddf_compact allocates its scratch per call (stream-ordered, on the
+ *    device that owns `flags`).
  *  - Return value: DDF_OK or an error class mirroring ddfield/errors.py;
  *    ddf_last_error() holds the message (thread-local).
  */
@@ -43,6 +44,9 @@ extern "C" {
 
 #define DDF_ENC_RAW5 0  /* neural.py:26-38 (x,y,z,az/pi-1,2pol/pi-1)      */
 #define DDF_ENC_PE6 1   /* + 6-octave sin/cos encoding -> 65 inputs (configs 3-5) */
+
+#define DDF_STAGE_STEPS 64    /* ddf_render_stats_t.primary_march_rows entries */
+#define DDF_STAGE_BOUNCES 32  /* ddf_render_stats_t.bounce_*_rows entries        */
 
 typedef struct ddf_field_s* ddf_field_t;
 
@@ -85,6 +89,19 @@ typedef struct {
      renders a pixel never changes its value (draws are addressed by global
      pixel index) */
   const int32_t* tile_owner;
+  /* nullable, debug: DEVICE int32 buffer of stage_log_cap words receiving
+     every compacted slot list of the render (the np.nonzero lists of
+     render.py:225 and field.py:277).  Word 0 = words written after the
+     2-word header, word 1 = 1 if a record did not fit.  Each record is
+     {kind, bounce, step, s0, n_own, count, count slot ids}: kind 0 = primary
+     march step, 1 = paths alive on entry to a bounce (after roulette; bucketed
+     by object for composite fields), 2 = bounce-ray march step, 3 = the part
+     of a bounce-ray march step 0 run by the fused trace+gradient kernel (kind
+     2 of the same step holds the rest).  Slot id = (s - s0) * n_own + k for
+     sample s of the wave starting at sample s0 and the k-th owned pixel.
+     Setting it disables the CUDA-graph replay. */
+  int32_t* stage_log;
+  int64_t stage_log_cap;
 } ddf_path_config_t;
 
 typedef struct {
@@ -114,6 +131,14 @@ typedef struct {
      kernel's launches and (profile = 1) time */
   uint64_t fused_rows, gradient_rows_executed, fused_launches;
   double ms_fused;
+  /* per-stage row counts summed over spp (the lengths of the np.nonzero
+     lists of render.py:225 and field.py:277): rows alive at primary march
+     step j, rows alive on entry to bounce b (after roulette), and forward
+     rows of bounce b's trace over all its march steps.  Steps and bounces
+     past the array ends are not recorded. */
+  uint64_t primary_march_rows[DDF_STAGE_STEPS];
+  uint64_t bounce_alive_rows[DDF_STAGE_BOUNCES];
+  uint64_t bounce_march_rows[DDF_STAGE_BOUNCES];
 } ddf_render_stats_t;
 
 /* NeuralField.__init__ (field.py:231-237): delta, AABB bounds (lo xyz, hi xyz). */

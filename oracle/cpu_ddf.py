@@ -526,8 +526,10 @@ def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None,
     per pixel of the range (accum / spp, film summed in spp order).
 
     ``log`` (a list) receives, per spp, a dict with the ascending local
-    indices alive at each primary march step ("primary_march") and alive on
-    entry to each bounce ("bounce_alive"), for compaction parity.
+    indices alive at each primary march step ("primary_march"), alive on
+    entry to each bounce ("bounce_alive"), and alive at each march step of
+    each bounce's trace ("bounce_march", one list of steps per bounce), for
+    compaction parity (render.py:225, field.py:277).
     EXTENSIONS: per-object albedo for composite fields; Russian roulette."""
     if cfg.bounces < 1:
         raise ValueError("path mode needs bounces >= 1")
@@ -558,6 +560,7 @@ def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None,
         alive = hit.copy()
         pos = o
         stages = []
+        marches = []
         for b in range(cfg.bounces):
             u = block(RNG_TAG, draw_index(s, 1 + b, n_pix, cfg.bounces), 2)
             if cfg.rr_start >= 0 and b >= cfg.rr_start and alive.any():
@@ -576,7 +579,10 @@ def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None,
             hp = pos[idx] + t[idx, None] * d[idx] + 1e-6 * nrm
             thr[idx] *= cfg.albedo if alb is None else alb[obj[idx]]
             nd = cosine_dirs(nrm, u[idx])
-            tn, hn, on = fld.trace(hp, nd)
+            bl = [] if log is not None else None
+            tn, hn, on = fld.trace(hp, nd, bl)
+            if log is not None:
+                marches.append([idx[j] for j in bl])
             esc = idx[~hn]
             rad[esc] += thr[esc] * cfg.env
             alive[esc] = False
@@ -590,8 +596,21 @@ def render_path(fld: Field, cam: Cam, cfg: PathConfig, pix_range=None, log=None,
             alive = nxt
         accum += rad
         if log is not None:
-            log.append({"primary_march": tl, "bounce_alive": stages})
+            log.append({"primary_march": tl, "bounce_alive": stages, "bounce_march": marches})
     return accum / cfg.spp
+
+
+def stage_sequence(log):
+    """The per-stage list lengths of a render_path log in the order the
+    reference's render loop hands lists to the backend: (0, n) per march step
+    (field.py:277), (1, n) per bounce's alive list (render.py:225)."""
+    seq = []
+    for rec in log:
+        seq += [(0, len(lst)) for lst in rec["primary_march"]]
+        for alive, steps in zip(rec["bounce_alive"], rec["bounce_march"]):
+            seq.append((1, len(alive)))
+            seq += [(0, len(lst)) for lst in steps]
+    return seq
 
 
 def film_rgb(value, cam: Cam):

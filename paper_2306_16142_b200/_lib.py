@@ -28,6 +28,7 @@ DDF_OK, DDF_EUSAGE, DDF_EDATA, DDF_ENUMERIC, DDF_ECUDA = 0, 1, 2, 3, 4
 PREC_FP32, PREC_BF16, PREC_FP32_SIMT = 0, 1, 2
 PRECISIONS = {"fp32": PREC_FP32, "bf16": PREC_BF16, "fp32_simt": PREC_FP32_SIMT}
 ENC_RAW5, ENC_PE6 = 0, 1
+STAGE_STEPS, STAGE_BOUNCES = 64, 32     # DDF_STAGE_STEPS, DDF_STAGE_BOUNCES
 
 EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "ddf_field_set_precision",
            "ddf_last_error", "ddf_mlp_forward", "ddf_mlp_input_grad", "ddf_query", "ddf_trace",
@@ -70,7 +71,8 @@ class PathConfig_t(ctypes.Structure):
                 ("rr_state", ctypes.c_uint64 * 2), ("rr_inc", ctypes.c_uint64 * 2),
                 ("tile", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("max_wave_paths", ctypes.c_int64), ("profile", ctypes.c_int32), ("graph", ctypes.c_int32),
-                ("no_fuse", ctypes.c_int32), ("tile_owner", ctypes.POINTER(ctypes.c_int32))]
+                ("no_fuse", ctypes.c_int32), ("tile_owner", ctypes.POINTER(ctypes.c_int32)),
+                ("stage_log", ctypes.POINTER(ctypes.c_int32)), ("stage_log_cap", ctypes.c_int64)]
 
 
 class ModeConfig_t(ctypes.Structure):
@@ -86,7 +88,19 @@ class RenderStats_t(ctypes.Structure):
                 ("ms_forward", ctypes.c_double), ("ms_gradient", ctypes.c_double),
                 ("ms_compact", ctypes.c_double), ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("fused_rows", ctypes.c_uint64), ("gradient_rows_executed", ctypes.c_uint64),
-                ("fused_launches", ctypes.c_uint64), ("ms_fused", ctypes.c_double)]
+                ("fused_launches", ctypes.c_uint64), ("ms_fused", ctypes.c_double),
+                ("primary_march_rows", ctypes.c_uint64 * STAGE_STEPS),
+                ("bounce_alive_rows", ctypes.c_uint64 * STAGE_BOUNCES),
+                ("bounce_march_rows", ctypes.c_uint64 * STAGE_BOUNCES)]
+
+
+def stats_dict(st: RenderStats_t) -> dict:
+    """ddf_render_stats_t as a dict; the per-stage arrays become lists."""
+    out = {}
+    for k, _ in RenderStats_t._fields_:
+        v = getattr(st, k)
+        out[k] = list(v) if isinstance(v, ctypes.Array) else v
+    return out
 
 
 _lib = None

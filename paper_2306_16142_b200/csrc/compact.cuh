@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(NT) count_kernel(const uint8_t* __restrict__ f
 __global__ void __launch_bounds__(1024) scan_kernel(int* __restrict__ block_counts, int nblocks, int n_obj,
                                                     int* __restrict__ seg, int* __restrict__ count,
                                                     unsigned long long* __restrict__ rows_acc,
-                                                    unsigned long long* __restrict__ rows_acc2) {
+                                                    unsigned long long* __restrict__ rows_acc2,
+                                                    unsigned long long* __restrict__ rows_acc3) {
   __shared__ int part[1024];
   __shared__ int seg_base;
   if (threadIdx.x == 0) seg_base = 0;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(int* __restrict__ block_coun
     *count = seg_base;
     if (rows_acc) *rows_acc += (unsigned long long)seg_base;
     if (rows_acc2) *rows_acc2 += (unsigned long long)seg_base;
+    if (rows_acc3) *rows_acc3 += (unsigned long long)seg_base;
   }
 }
 
@@ -160,7 +162,8 @@ __global__ void __launch_bounds__(NT) onepass_kernel(const uint8_t* __restrict__
                                                      int sel_val, int n, int nb, unsigned long long* state,
                                                      int* __restrict__ list, int* __restrict__ seg,
                                                      int* __restrict__ count, unsigned long long* rows_acc,
-                                                     unsigned long long* rows_acc2) {
+                                                     unsigned long long* rows_acc2,
+                                                     unsigned long long* rows_acc3) {
   __shared__ int warp_tot[NT / 32];
   __shared__ int s_ticket, s_excl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -249,6 +252,7 @@ __global__ void __launch_bounds__(NT) onepass_kernel(const uint8_t* __restrict__
     *count = pos;
     if (rows_acc) *rows_acc += (unsigned long long)pos;
     if (rows_acc2) *rows_acc2 += (unsigned long long)pos;
+    if (rows_acc3) *rows_acc3 += (unsigned long long)pos;
   }
 }
 

@@ -132,9 +132,14 @@ namespace {
 // [0] forward rows, [1] gradient rows (reference count: rows needing a normal),
 // [2] degenerate normals, [3] fused trace+gradient rows, [4] rows of the
 // gradient pass proper when fusion is on
+// [16..) per-stage rows: primary march steps [16, 80), bounce alive [80, 112), bounce march [112, 144)
 struct Small {
   int* seg; int* count; int* count2; int* err; unsigned long long* stats;  // stats[0]=fwd [1]=grad [2]=degenerate
+  unsigned long long* primary_rows() const { return stats + 16; }
+  unsigned long long* alive_rows() const { return stats + 16 + DDF_STAGE_STEPS; }
+  unsigned long long* bmarch_rows() const { return stats + 16 + DDF_STAGE_STEPS + DDF_STAGE_BOUNCES; }
 };
+constexpr int SMALL_U64 = 16 + DDF_STAGE_STEPS + 2 * DDF_STAGE_BOUNCES;   // u64 stats words in use
 Small small_of(ddf_field_s* f) {
   Small s;
   int* b = f->small.as<int>();
@@ -250,7 +255,7 @@ int run_fused(ddf_field_s* f, const TraceGradOp& op, int max_rows, cudaStream_t 
 // stable compaction flags -> list (+ segments by object when obj != nullptr)
 int compact_flags(ddf_field_s* f, const uint8_t* flags, const int* obj, int n, int n_obj, int* list, int* seg,
                   int* count, unsigned long long* rows_acc, cudaStream_t st, const uint8_t* sel = nullptr,
-                  int sel_val = 0, unsigned long long* rows_acc2 = nullptr) {
+                  int sel_val = 0, unsigned long long* rows_acc2 = nullptr, unsigned long long* rows_acc3 = nullptr) {
   const int nb = std::max(1, (n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS);
   CUDA_TRY(f->blocks.ensure(std::max(sizeof(int) * nb * DDF_MAX_OBJECTS, sizeof(unsigned long long) * (nb + 1))));
   int* bc = f->blocks.as<int>();
@@ -262,13 +267,13 @@ int compact_flags(ddf_field_s* f, const uint8_t* flags, const int* obj, int n, i
     CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb1 + 1), st));
     f->prof.launches += 1;
     compact::onepass_kernel<<<nb1, compact::NT, 0, st>>>(flags, sel, sel_val, n, nb1, state, list, seg, count,
-                                                          rows_acc, rows_acc2);
+                                                          rows_acc, rows_acc2, rows_acc3);
     CUDA_TRY(cudaGetLastError());
     return DDF_OK;
   }
   f->prof.launches += 3;
   compact::count_kernel<<<nb, compact::NT, 0, st>>>(flags, sel, sel_val, obj, n, no, bc);
-  compact::scan_kernel<<<1, 1024, 0, st>>>(bc, nb, no, seg, count, rows_acc, rows_acc2);
+  compact::scan_kernel<<<1, 1024, 0, st>>>(bc, nb, no, seg, count, rows_acc, rows_acc2, rows_acc3);
   compact::scatter_kernel<<<nb, compact::NT, 0, st>>>(flags, sel, sel_val, obj, n, no, bc, list);
   CUDA_TRY(cudaGetLastError());
   return DDF_OK;
@@ -289,24 +294,75 @@ __global__ void trace_init_kernel(const FieldDev F, MarchState S, int n) {
   if (S.obj) S.obj[i] = 0;
 }
 
+// stage log (ddf_path_config_t.stage_log): appends one compacted list as
+// {kind, bounce, step, s0, n_own, count, ids...}.  Every block reads the same
+// header word; the commit kernel that follows advances it.
+struct StageLog {
+  int* log = nullptr;
+  long long cap = 0;
+  int s0 = 0, n_own = 0;
+};
+
+__global__ void stage_log_copy_kernel(int* __restrict__ log, long long cap, const int* __restrict__ list,
+                                      const int* __restrict__ count, int kind, int bounce, int step, int s0,
+                                      int n_own) {
+  const long long used = log[0];
+  const int n = *count;
+  if (log[1] || 2 + used + 6 + n > cap) return;
+  int* rec = log + 2 + used;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rec[0] = kind; rec[1] = bounce; rec[2] = step; rec[3] = s0; rec[4] = n_own; rec[5] = n;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) rec[6 + i] = list[i];
+}
+
+__global__ void stage_log_commit_kernel(int* log, long long cap, const int* count) {
+  const long long need = 6 + (long long)*count;
+  if (log[1] || 2 + (long long)log[0] + need > cap) log[1] = 1;
+  else log[0] += (int)need;
+}
+
+int stage_log(ddf_field_s* f, const StageLog* lg, const int* list, const int* count, int kind, int bounce, int step,
+              cudaStream_t st) {
+  if (!lg || !lg->log) return DDF_OK;
+  stage_log_copy_kernel<<<2 * f->sm_count, 256, 0, st>>>(lg->log, lg->cap, list, count, kind, bounce, step, lg->s0,
+                                                         lg->n_own);
+  stage_log_commit_kernel<<<1, 1, 0, st>>>(lg->log, lg->cap, count);
+  f->prof.launches += 2;
+  CUDA_TRY(cudaGetLastError());
+  return DDF_OK;
+}
+
 // sphere march over the slots whose `march` flag is set (field.py:274-288)
 // fused (nullable): step 0 of the rows whose `want` byte is set runs as
-// TraceGradOp (fused normal reuse); the other rows take the plain step
+// TraceGradOp (fused normal reuse); the other rows take the plain step.
+// step_rows (nullable): per-stage row counters, entry step * step_stride
+// (stride 1: one counter per march step; 0: one counter for the whole march,
+// ddf_render_stats_t.primary_march_rows / bounce_march_rows).  lg / bounce:
+// the stage log (kind 0 for bounce < 0, else kinds 2 and 3).
 int march(ddf_field_s* f, const MarchState& ms, int n, int* list, unsigned long long* fwd_acc, cudaStream_t st,
-          const TraceGradOp* fused = nullptr, const uint8_t* want = nullptr) {
+          const TraceGradOp* fused = nullptr, const uint8_t* want = nullptr,
+          unsigned long long* step_rows = nullptr, int step_stride = 0, const StageLog* lg = nullptr,
+          int bounce = -1) {
   Small sm = small_of(f);
   for (int step = 0; step < f->F.max_steps; ++step) {
     const bool fz = fused && step == 0;
+    unsigned long long* srow =
+        step_rows && (step_stride == 0 || step < DDF_STAGE_STEPS) ? step_rows + step * step_stride : nullptr;
     if (fz) {
-      int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st, want, 1, sm.stats + 3);
+      int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st, want, 1, sm.stats + 3,
+                             srow);
       if (rc) return rc;
+      if ((rc = stage_log(f, lg, list, sm.count, 3, bounce, step, st))) return rc;
       TraceGradOp op = *fused;
       op.list = list; op.count = sm.count; op.n = n; op.seg = nullptr;
       op.st = ms; op.delta = f->F.delta; op.thresh = f->F.thresh; op.step = f->F.step;
       if ((rc = run_fused(f, op, n, st))) return rc;
     }
-    int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st, fz ? want : nullptr, 0);
+    int rc = compact_flags(f, ms.alive, nullptr, n, 1, list, sm.seg, sm.count, fwd_acc, st, fz ? want : nullptr, 0,
+                           srow);
     if (rc) return rc;
+    if ((rc = stage_log(f, lg, list, sm.count, bounce < 0 ? 0 : 2, bounce, step, st))) return rc;
     TraceStepOp op{};
     op.list = list; op.count = sm.count; op.n = n; op.seg = nullptr;
     op.st = ms; op.delta = f->F.delta; op.thresh = f->F.thresh; op.step = f->F.step;
@@ -929,6 +985,13 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   w.rng = f->rng.as<PcgStream>(); w.rr = f->rng.as<PcgStream>() + 1;
   w.err = sm.err; w.degenerate = sm.stats + 2;
 
+  // stage log (debug): the header is cleared once per render
+  const bool lg_on = cfg->stage_log != nullptr;
+  if (lg_on && cfg->stage_log_cap < 2) return fail(DDF_EUSAGE, "stage_log needs at least 2 words");
+  StageLog lg;
+  lg.log = cfg->stage_log; lg.cap = cfg->stage_log_cap; lg.n_own = n_own;
+  if (lg_on) CUDA_TRY(cudaMemsetAsync(lg.log, 0, 2 * sizeof(int), st));
+
   int waves = 0;
   // the wave loop: stream-ordered launches only (no host syncs, no
   // allocations once the buffers have grown), so it can be captured
@@ -936,6 +999,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     waves = 0;
     for (int s0 = 0; s0 < cfg->spp; s0 += ns) {
       w.s0 = s0;
+      lg.s0 = s0;
       w.ns = std::min(ns, cfg->spp - s0);
       const int Pw = w.ns * n_own;
       const int g = (Pw + 255) / 256;
@@ -950,7 +1014,8 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
         mesh::trace_paths_kernel<<<g, 256, 0, ss>>>(f->M, S, nullptr, nullptr, Pw);
         f->prof.launches += 1;
         f->prof.fwd_launches += 1;
-      } else if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, ss)) {
+      } else if (int rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, ss, nullptr, nullptr,
+                                sm.primary_rows(), 1, lg_on ? &lg : nullptr, -1)) {
         return rc;
       }
       {
@@ -965,8 +1030,10 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
           f->prof.launches += 1;
         }
         int rc = compact_flags(f, S.alive, f->F.n_obj > 1 ? S.obj : nullptr, Pw, f->F.n_obj, f->list.as<int>(),
-                               sm.seg, sm.count2, sm.stats + 1, ss);
+                               sm.seg, sm.count2, sm.stats + 1, ss, nullptr, 0,
+                               b < DDF_STAGE_BOUNCES ? sm.alive_rows() + b : nullptr);
         if (rc) return rc;
+        if ((rc = stage_log(f, lg_on ? &lg : nullptr, f->list.as<int>(), sm.count2, 1, b, 0, ss))) return rc;
         if (f->F.is_mesh) {
           ProfScope ps(f->prof, Prof::GRAD, ss);
           mesh::face_normal_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(f->M, S, f->list.as<int>(), sm.count2);
@@ -1000,7 +1067,9 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
           f->prof.launches += 1;
           f->prof.fwd_launches += 1;
         } else if ((rc = march(f, ms, Pw, f->list2.as<int>(), sm.stats + 0, ss,
-                               fuse && b + 1 < cfg->bounces ? &tg : nullptr, S.want))) {
+                               fuse && b + 1 < cfg->bounces ? &tg : nullptr, S.want,
+                               b < DDF_STAGE_BOUNCES ? sm.bmarch_rows() + b : nullptr, 0, lg_on ? &lg : nullptr,
+                               b))) {
           return rc;
         }
         {
@@ -1021,7 +1090,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   };
   // CUDA graph replay (cfg->graph): the captured loop is keyed by the field
   // generation, the buffer epoch, the camera, the config and the accumulator
-  const bool use_graph = cfg->graph != 0 && !f->prof.on;
+  const bool use_graph = cfg->graph != 0 && !f->prof.on && !lg_on;
   std::vector<unsigned char> gkey;
   if (use_graph) {
     ddf_path_config_t kc = *cfg;
@@ -1033,6 +1102,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     put(&gen, sizeof gen);
     put(cam, sizeof(*cam));
     kc.tile_owner = nullptr;   // the table's contents, not its address, key the graph
+    kc.stage_log = nullptr;
     put(&kc, sizeof kc);
     put(&acc, sizeof acc);
     if (!owner.empty()) put(owner.data(), sizeof(int32_t) * owner.size());
@@ -1081,7 +1151,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     }
   }
   if (f->prof.on) f->prof.marks[Prof::TOTAL].push_back({t_begin, f->prof.rec(st)});
-  int host_small[32 + 10];
+  int host_small[32 + 2 * SMALL_U64];
   CUDA_TRY(cudaMemcpyAsync(host_small, f->small.p, sizeof(host_small), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   const unsigned long long* hs64 = reinterpret_cast<const unsigned long long*>(host_small + 32);
@@ -1103,6 +1173,11 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     stats->ms_compact = f->prof.total_ms(Prof::COMPACT);
     stats->ms_other = f->prof.total_ms(Prof::OTHER);
     stats->ms_total = f->prof.total_ms(Prof::TOTAL);
+    for (int j = 0; j < DDF_STAGE_STEPS; ++j) stats->primary_march_rows[j] = hs64[16 + j];
+    for (int b = 0; b < DDF_STAGE_BOUNCES; ++b) {
+      stats->bounce_alive_rows[b] = hs64[16 + DDF_STAGE_STEPS + b];
+      stats->bounce_march_rows[b] = hs64[16 + DDF_STAGE_STEPS + DDF_STAGE_BOUNCES + b];
+    }
   }
   if (host_small[18] & DEVERR_SIGN_RULE) return fail(DDF_ENUMERIC, "normal sign rule violated: n . dir >= 0");
   return DDF_OK;
@@ -1194,10 +1269,6 @@ __global__ void rng_kernel(const PcgStream* st, const uint64_t* idx, int n, doub
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) out[j] = pcg_single(*st, idx[j]);
 }
-struct CompactScratch {
-  Buf blocks, seg;
-};
-CompactScratch g_cs;
 }  // namespace
 
 int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64_t* idx, int64_t n, double* out,
@@ -1231,15 +1302,23 @@ int ddf_debug_counters(uint64_t* out16, int32_t reset) {
 int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, void* stream) {
   if (n < 0 || n > (1ll << 30)) return fail(DDF_EUSAGE, "bad count");
   cudaStream_t st = (cudaStream_t)stream;
-  const int nb = std::max<int>(1, (int)((n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS));
-  CUDA_TRY(g_cs.blocks.ensure(sizeof(unsigned long long) * (nb + 1)));
-  CUDA_TRY(g_cs.seg.ensure(sizeof(int) * 2));
+  // scratch is stream-ordered and per call, on the device that owns `flags`
+  // (no process-wide buffers, nothing a captured render graph refers to)
+  cudaPointerAttributes pa{};
+  if (n > 0) {
+    CUDA_TRY(cudaPointerGetAttributes(&pa, flags));
+    if (pa.type == cudaMemoryTypeDevice) CUDA_TRY(cudaSetDevice(pa.device));
+  }
   const int nb1 = std::max<int>(1, (int)((n + compact::OP_ITEMS - 1) / compact::OP_ITEMS));
-  unsigned long long* state = g_cs.blocks.as<unsigned long long>();
+  unsigned long long* state = nullptr;
+  const size_t bytes = sizeof(unsigned long long) * (nb1 + 1) + 2 * sizeof(int);
+  CUDA_TRY(cudaMallocAsync((void**)&state, bytes, st));
   CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb1 + 1), st));
-  compact::onepass_kernel<<<nb1, compact::NT, 0, st>>>(flags, nullptr, 0, (int)n, nb1, state, list,
-                                                        g_cs.seg.as<int>(), count, nullptr, nullptr);
+  int* seg = reinterpret_cast<int*>(state + nb1 + 1);
+  compact::onepass_kernel<<<nb1, compact::NT, 0, st>>>(flags, nullptr, 0, (int)n, nb1, state, list, seg, count,
+                                                        nullptr, nullptr, nullptr);
   CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(state, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return DDF_OK;
 }

@@ -15,6 +15,7 @@ albedos)`` composes several networks by min distance.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import numpy as np
@@ -37,26 +38,35 @@ def _dev(a, dtype=torch.float64, device="cuda"):
     return t.to(device, non_blocking=True)
 
 
-def _host(*ts):
-    """Device tensors -> numpy through pinned buffers: asynchronous copies on
-    the current stream and one synchronize (a pageable .cpu() per output pays
-    a staged copy and a sync each).  The arrays view their pinned tensors,
-    which they keep alive."""
+PINNED_READBACK_BYTES = 8 << 20
+
+
+def _host(stream, *ts):
+    """Device tensors -> numpy, ordered on ``stream`` (the field's device).
+    Small results (<= 8 MB in all) go through pinned buffers: asynchronous
+    copies and one synchronize, the blocks recycled by PyTorch's host
+    allocator.  Larger ones use pageable copies, so a big protocol call does
+    not leave page-locked memory behind.  The arrays are plain numpy either
+    way, as the reference returns."""
+    if sum(t.numel() * t.element_size() for t in ts) > PINNED_READBACK_BYTES:
+        with torch.cuda.stream(stream):
+            return [t.cpu().numpy() for t in ts]
     outs = []
     for t in ts:
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-        h.copy_(t, non_blocking=True)
+        with torch.cuda.stream(stream):
+            h.copy_(t, non_blocking=True)
         outs.append(h)
-    torch.cuda.current_stream().synchronize()
-    return [h.numpy() for h in outs]
+    stream.synchronize()
+    return [np.array(h.numpy()) for h in outs]
 
 
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
-def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 class CudaNeuralField:
@@ -144,6 +154,14 @@ class CudaNeuralField:
         return self._h
 
     # ------------------------------------------------------------ protocol
+    @contextlib.contextmanager
+    def _call(self):
+        """Make the field's device current for one protocol call (restored
+        afterwards, so a C call's cudaSetDevice does not leak) and yield that
+        device's current stream."""
+        with torch.cuda.device(self.torch_device):
+            yield torch.cuda.current_stream(self.torch_device)
+
     def _rows(self, *arrays):
         n = None
         out = []
@@ -156,33 +174,39 @@ class CudaNeuralField:
             out.append(a)
         return n, out
 
+    def _empty(self, shape, dtype=torch.float64):
+        return torch.empty(shape, dtype=dtype, device=self.torch_device)
+
     def forward_inputs(self, inputs, net: int = 0):
         """neural.forward_batch (neural.py:138-157) on raw network inputs."""
         x = np.atleast_2d(np.asarray(inputs, dtype=np.float64))
-        xd = _dev(x, device=self.torch_device)
-        out = torch.empty(len(x), dtype=torch.float64, device=self.torch_device)
-        _lib.check(_lib.lib().ddf_mlp_forward(self._h, net, _ptr(xd), len(x), _ptr(out), _stream()))
-        return _host(out)[0]
+        with self._call() as st:
+            xd = _dev(x, device=self.torch_device)
+            out = self._empty(len(x))
+            _lib.check(_lib.lib().ddf_mlp_forward(self._h, net, _ptr(xd), len(x), _ptr(out),
+                                                  ctypes.c_void_p(st.cuda_stream)))
+            return _host(st, out)[0]
 
     def input_gradient_inputs(self, inputs, net: int = 0):
         """neural.input_gradient_batch (neural.py:229-249) on raw inputs."""
         x = np.atleast_2d(np.asarray(inputs, dtype=np.float64))
-        xd = _dev(x, device=self.torch_device)
-        out = torch.empty(x.shape, dtype=torch.float64, device=self.torch_device)
-        _lib.check(_lib.lib().ddf_mlp_input_grad(self._h, net, _ptr(xd), len(x), _ptr(out), _stream()))
-        return _host(out)[0]
+        with self._call() as st:
+            xd = _dev(x, device=self.torch_device)
+            out = self._empty(x.shape)
+            _lib.check(_lib.lib().ddf_mlp_input_grad(self._h, net, _ptr(xd), len(x), _ptr(out),
+                                                     ctypes.c_void_p(st.cuda_stream)))
+            return _host(st, out)[0]
 
     def query_raw(self, positions, dir_vecs):
         """(pred, t, hit, obj): the raw network distance next to query_batch."""
         n, (p, d) = self._rows(positions, dir_vecs)
-        pd, dd = _dev(p, device=self.torch_device), _dev(d, device=self.torch_device)
-        t = torch.empty(n, dtype=torch.float64, device=self.torch_device)
-        pred = torch.empty(n, dtype=torch.float64, device=self.torch_device)
-        hit = torch.empty(n, dtype=torch.uint8, device=self.torch_device)
-        obj = torch.empty(n, dtype=torch.int32, device=self.torch_device)
-        _lib.check(_lib.lib().ddf_query(self._h, _ptr(pd), _ptr(dd), n, _ptr(t), _ptr(hit), _ptr(pred), _ptr(obj),
-                                        _stream()))
-        pred, t, hit, obj = _host(pred, t, hit, obj)
+        with self._call() as st:
+            pd, dd = _dev(p, device=self.torch_device), _dev(d, device=self.torch_device)
+            t, pred = self._empty(n), self._empty(n)
+            hit, obj = self._empty(n, torch.uint8), self._empty(n, torch.int32)
+            _lib.check(_lib.lib().ddf_query(self._h, _ptr(pd), _ptr(dd), n, _ptr(t), _ptr(hit), _ptr(pred),
+                                            _ptr(obj), ctypes.c_void_p(st.cuda_stream)))
+            pred, t, hit, obj = _host(st, pred, t, hit, obj)
         return pred, t, hit.astype(bool), obj
 
     def query_batch(self, positions, dir_vecs):
@@ -198,13 +222,14 @@ class CudaNeuralField:
         return self.query_batch(positions, d)
 
     def trace_with_objects(self, origins, dir_vecs):
+        """trace_batch plus the id of the object each ray hit (0 for one net)."""
         n, (o, d) = self._rows(origins, dir_vecs)
-        od, dd = _dev(o, device=self.torch_device), _dev(d, device=self.torch_device)
-        t = torch.empty(n, dtype=torch.float64, device=self.torch_device)
-        hit = torch.empty(n, dtype=torch.uint8, device=self.torch_device)
-        obj = torch.empty(n, dtype=torch.int32, device=self.torch_device)
-        _lib.check(_lib.lib().ddf_trace(self._h, _ptr(od), _ptr(dd), n, _ptr(t), _ptr(hit), _ptr(obj), _stream()))
-        t, hit, obj = _host(t, hit, obj)
+        with self._call() as st:
+            od, dd = _dev(o, device=self.torch_device), _dev(d, device=self.torch_device)
+            t, hit, obj = self._empty(n), self._empty(n, torch.uint8), self._empty(n, torch.int32)
+            _lib.check(_lib.lib().ddf_trace(self._h, _ptr(od), _ptr(dd), n, _ptr(t), _ptr(hit), _ptr(obj),
+                                            ctypes.c_void_p(st.cuda_stream)))
+            t, hit, obj = _host(st, t, hit, obj)
         return t, hit.astype(bool), obj
 
     def trace_batch(self, origins, dir_vecs):
@@ -213,27 +238,35 @@ class CudaNeuralField:
         return t, hit
 
     def normal_batch(self, origins, dir_vecs, t_hit=None, obj=None):
-        """field.py:295-317 -> (normals, valid)."""
+        """field.py:295-317 -> (normals, valid).
+
+        Composite fields (config 5) take the gradient of one object per row:
+        ``obj`` (the hit object from trace_with_objects) when given.  Called
+        through the plain protocol, as the reference's render loop does
+        (render.py:131), there is no object id, so the row's object is the
+        scene's argmin at the evaluation point itself."""
         n, (o, d) = self._rows(origins, dir_vecs)
-        od, dd = _dev(o, device=self.torch_device), _dev(d, device=self.torch_device)
-        th = _dev(np.asarray(t_hit, dtype=np.float64).reshape(n), device=self.torch_device) if t_hit is not None else None
-        ob = _dev(np.asarray(obj).reshape(n), dtype=torch.int32, device=self.torch_device) if obj is not None else None
-        nr = torch.empty((n, 3), dtype=torch.float64, device=self.torch_device)
-        valid = torch.empty(n, dtype=torch.uint8, device=self.torch_device)
-        _lib.check(_lib.lib().ddf_normal(self._h, _ptr(od), _ptr(dd), _ptr(th), _ptr(ob), n, _ptr(nr), _ptr(valid),
-                                         _stream()))
-        nr, valid = _host(nr, valid)
+        th = None if t_hit is None else np.asarray(t_hit, dtype=np.float64).reshape(n)
+        if obj is None and self.albedos is not None and n:
+            back = np.zeros(n) if th is None else np.maximum(th - self.normal_eval_backoff, 0.0)
+            _, _, _, obj = self.query_raw(o + back[:, None] * d, d)
+        with self._call() as st:
+            od, dd = _dev(o, device=self.torch_device), _dev(d, device=self.torch_device)
+            thd = _dev(th, device=self.torch_device) if th is not None else None
+            ob = _dev(np.asarray(obj).reshape(n), dtype=torch.int32, device=self.torch_device) if obj is not None \
+                else None
+            nr, valid = self._empty((n, 3)), self._empty(n, torch.uint8)
+            _lib.check(_lib.lib().ddf_normal(self._h, _ptr(od), _ptr(dd), _ptr(thd), _ptr(ob), n, _ptr(nr),
+                                             _ptr(valid), ctypes.c_void_p(st.cuda_stream)))
+            nr, valid = _host(st, nr, valid)
         return nr, valid.astype(bool)
 
     def input_gradients(self, positions, angles):
         """field.py:291-293: (N, 5) gradient w.r.t. the encoded inputs
         (single-network fields, reference encoding)."""
-        p = np.atleast_2d(np.asarray(positions, dtype=np.float64))
-        a = np.atleast_2d(np.asarray(angles, dtype=np.float64))
-        x = np.empty((len(p), 5))
-        x[:, :3] = p
-        x[:, 3] = a[:, 0] / np.pi - 1.0
-        x[:, 4] = 2.0 * a[:, 1] / np.pi - 1.0
         if int(self.model.widths[0]) != 5:
             raise ValueError("input_gradients on raw inputs needs a 5-input network")
+        p = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+        a = np.atleast_2d(np.asarray(angles, dtype=np.float64))
+        x = np.concatenate([p, a[:, :1] / np.pi - 1.0, 2.0 * a[:, 1:2] / np.pi - 1.0], axis=1)  # neural.py:26-38
         return self.input_gradient_inputs(x)

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .field import _dev, _ptr, _stream
+from .field import _dev, _ptr
 
 
 @dataclass
@@ -87,8 +87,9 @@ def udf_many(backend, points, n_dirs: int = 512, exact: bool | None = None, poli
         return backend.exact_distance(pts)
     if len(pts) == 0:
         return np.empty(0)
-    d = _dev(pts, device=backend.torch_device)
-    return udf_many_device(backend, d, n_dirs, polish).cpu().numpy()
+    with torch.cuda.device(backend.torch_device):
+        d = _dev(pts, device=backend.torch_device)
+        return udf_many_device(backend, d, n_dirs, polish).cpu().numpy()
 
 
 def udf(backend, x, n_dirs: int = 512, exact: bool | None = None, polish: bool = True):
@@ -109,8 +110,10 @@ def udf_grid(backend, resolution: int = 64, n_dirs: int = 512, bounds=None, exac
     box = np.asarray(bounds if bounds is not None else backend.grid_bounds, dtype=np.float64).reshape(2, 3)
     if _exact(backend, exact) and not getattr(backend, "exact_udf", False):
         return ScalarGrid(box, backend.exact_distance(grid_points(box, resolution)).reshape((resolution,) * 3))
-    out = torch.empty(resolution ** 3, dtype=torch.float64, device=backend.torch_device)
-    b6 = (ctypes.c_double * 6)(*box.reshape(-1))
-    _lib.check(_lib.lib().ddf_udf_grid(backend.handle, b6, int(resolution), int(n_dirs), int(bool(polish)),
-                                       _ptr(out), _stream()))
-    return ScalarGrid(box, out.cpu().numpy().reshape(resolution, resolution, resolution))
+    with torch.cuda.device(backend.torch_device):
+        out = torch.empty(resolution ** 3, dtype=torch.float64, device=backend.torch_device)
+        b6 = (ctypes.c_double * 6)(*box.reshape(-1))
+        st = torch.cuda.current_stream(backend.torch_device)
+        _lib.check(_lib.lib().ddf_udf_grid(backend.handle, b6, int(resolution), int(n_dirs), int(bool(polish)),
+                                           _ptr(out), ctypes.c_void_p(st.cuda_stream)))
+        return ScalarGrid(box, out.cpu().numpy().reshape(resolution, resolution, resolution))

@@ -7,7 +7,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-REFERENCE_SRC = "/root/reference/pkg/src"
+# The unmodified reference, importable as ``ddfield``: the offline install in
+# baseline/_ref (travels to the GPU box with the repo snapshot), else the
+# read-only source tree of the build container.
+REFERENCE_PATHS = (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src")
 
 
 def pytest_configure(config):
@@ -21,15 +24,24 @@ def golden():
     return np.load(os.path.join(ROOT, "tests", "golden", "reference_golden.npz"))
 
 
+def _reference_path():
+    for p in REFERENCE_PATHS:
+        if os.path.isdir(os.path.join(p, "ddfield")):
+            return p
+    return None
+
+
 @pytest.fixture(scope="session")
 def reference():
-    """The live reference package, only where /root/reference exists (the
-    build container); GPU boxes skip these checks and use the fixtures."""
-    if not os.path.isdir(REFERENCE_SRC):
-        pytest.skip("reference source not present (GPU box): fixtures only")
+    """The live reference package (neural, field, render modules).  It is a
+    checker only: the product never imports it."""
+    path = _reference_path()
+    if path is None:
+        pytest.skip("reference not installed (python -m pip install --no-index --no-build-isolation --no-deps "
+                    "--target baseline/_ref <copy of /root/reference/pkg>)")
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
-    if REFERENCE_SRC not in sys.path:
-        sys.path.insert(0, REFERENCE_SRC)
+    if path not in sys.path:
+        sys.path.insert(0, path)
     try:
         from ddfield import field, neural, render
     except Exception as exc:  # numba missing etc.

@@ -1,6 +1,7 @@
-"""Multi-rank host logic on CPU (gloo, world size 2): tile ownership, per-rank
-renders of owned tiles (CPU oracle stands in for each rank's GPU), and the
-single all-reduce of the film reproduce the 1-rank film bit-exactly."""
+"""Multi-rank host logic on CPU (gloo, world sizes 2 and 8): tile ownership,
+per-rank renders of owned tiles (the CPU oracle stands in for each rank's
+GPU), the pilot's cost sum and the single film reduce to rank 0 reproduce the
+1-rank film bit-exactly."""
 
 import os
 import socket
@@ -12,7 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import cpu_ddf as O
-from paper_2306_16142_b200.dist import balanced_tile_owners, owned_pixels
+from paper_2306_16142_b200.dist import balanced_tile_owners, owned_pixels, reduce_film
 
 W, H, TILE = 24, 16, 8
 
@@ -24,17 +25,30 @@ def _field_cam():
     return f, cam, O.PathConfig(spp=2, bounces=3, albedo=0.7, env=1.0, seed=42, rr_start=1)
 
 
-def _worker(rank, world, port, out, owner=None):
+def _worker(rank, world, port, out, owner=None, pilot=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     f, cam, cfg = _field_cam()
+    if pilot:
+        # dist.balanced_owners_distributed's exchange: each rank costs its
+        # round-robin tiles (here: owned path samples x alive rows of a 1-spp
+        # oracle render), one sum makes the vector identical on every rank
+        ntx, nty = -(-W // TILE), -(-H // TILE)
+        cost = torch.zeros(ntx * nty, dtype=torch.float64)
+        for k in range(rank, ntx * nty, world):
+            px = owned_pixels(W, H, TILE, k, ntx * nty)
+            cost[k] = float(np.sum(O.render_path(f, cam, O.PathConfig(spp=1, bounces=3, seed=42), pixels=px) > 0))
+            cost[k] += 1.0 + k % 3
+        dist.all_reduce(cost, op=dist.ReduceOp.SUM)
+        owner = balanced_tile_owners(cost.numpy(), world)
+        out.put(("owner", rank, owner.tobytes()))
     mine = owned_pixels(W, H, TILE, rank, world, owner)
     film = torch.zeros(W * H, dtype=torch.float64)
     film[torch.from_numpy(mine)] = torch.from_numpy(O.render_path(f, cam, cfg, pixels=mine))
-    dist.all_reduce(film, op=dist.ReduceOp.SUM)
+    reduce_film(film)
     if rank == 0:
-        out.put(film.numpy().tobytes())
+        out.put(("film", rank, film.numpy().tobytes()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -86,8 +100,9 @@ def test_balanced_tile_owners_lpt():
         assert len(allp) == 1920 * 1080 and len(np.unique(allp)) == 1920 * 1080
 
 
-@pytest.mark.parametrize("balanced", [False, True])
-def test_gloo_world2_film_allreduce_is_exact(balanced):
+@pytest.mark.parametrize("world,balanced,pilot", [(2, False, False), (2, True, False), (8, False, False),
+                                                  (8, False, True)])
+def test_gloo_film_reduce_is_exact(world, balanced, pilot):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -95,12 +110,20 @@ def test_gloo_world2_film_allreduce_is_exact(balanced):
     if balanced:   # a skewed table from a made-up cost: one heavy tile alone on rank 0
         owner = balanced_tile_owners(np.array([9.0, 1.0, 1.0, 1.0, 1.0, 1.0]), 2)
         assert list(np.bincount(owner)) == [1, 5]
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, owner)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, owner, pilot)) for r in range(world)]
     for p in procs:
         p.start()
-    got = np.frombuffer(q.get(timeout=300), dtype=np.float64)
+    msgs = [q.get(timeout=300) for _ in range(1 + (world if pilot else 0))]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    films = [m for m in msgs if m[0] == "film"]
+    assert len(films) == 1 and films[0][1] == 0
+    got = np.frombuffer(films[0][2], dtype=np.float64)
+    if pilot:   # every rank derived the same table; 6 tiles land on 6 distinct ranks
+        tables = {np.frombuffer(m[2], dtype=np.int32).tobytes() for m in msgs if m[0] == "owner"}
+        assert len(tables) == 1
+        n_tiles = -(-W // TILE) * -(-H // TILE)
+        assert set(np.frombuffer(tables.pop(), dtype=np.int32)) == set(range(min(world, n_tiles)))
     f, cam, cfg = _field_cam()
     assert np.array_equal(got, O.render_path(f, cam, cfg))

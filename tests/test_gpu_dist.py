@@ -1,8 +1,8 @@
 """dist.render_path_distributed with a real 2-rank process group.
 
 Both ranks share cuda:0 (the test box has one GPU) and reduce over gloo; the
-ranks' kernels never wait on each other, only the host-side all-reduce does.
-The reduced film must equal the 1-rank film bit-exactly."""
+ranks' kernels never wait on each other, only the host-side reduce does.
+The film reduced onto rank 0 must equal the 1-rank film bit-exactly."""
 
 import os
 import socket
@@ -21,25 +21,27 @@ import torch.multiprocessing as mp  # noqa: E402
 W, H = 150, 70
 
 
-def _setup(precision):
+def _setup(precision, tile=0):
     from paper_2306_16142_b200 import render as R
     from paper_2306_16142_b200.field import CudaNeuralField
     from paper_2306_16142_b200.neural import kaiming_uniform
     net = kaiming_uniform((65, 128, 128, 1), 6)
     f = CudaNeuralField(net, 10.0 / 0.98, bounds=np.array([[-1.0] * 3, [1.0] * 3]), precision=precision)
     cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=W, height=H)
-    cfg = R.RenderConfig(spp=2, bounces=3, seed=5, rr_start=1)
+    cfg = R.RenderConfig(spp=2, bounces=3, seed=5, rr_start=1, tile=tile)
     return f, cam, cfg
 
 
-def _worker(rank, world, port, precision, out, tile_owner=None):
+def _worker(rank, world, port, precision, out, tile_owner=None, tile=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2306_16142_b200.dist import render_path_distributed
-    f, cam, cfg = _setup(precision)
+    f, cam, cfg = _setup(precision, tile)
     fb, stats = render_path_distributed(f, cam, cfg, tile_owner=tile_owner)
-    out.put((rank, np.asarray(fb.data).tobytes(), int(stats["path_samples"])))
+    assert (fb is None) == (rank != 0)
+    out.put((rank, None if fb is None else np.asarray(fb.data).tobytes(), int(stats["path_samples"]),
+             stats.get("pilot_s")))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -50,13 +52,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("precision,balance", [("fp32", None), ("bf16", None), ("bf16", "balanced")])
-def test_two_rank_render_equals_single_rank(precision, balance):
+@pytest.mark.parametrize("precision,balance,tile", [("fp32", None, 0), ("bf16", None, 0), ("bf16", "balanced", 0),
+                                                   ("bf16", "balanced", 32)])
+def test_two_rank_render_equals_single_rank(precision, balance, tile):
     from paper_2306_16142_b200 import render as R
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, precision, q, balance)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, precision, q, balance, tile)) for r in range(2)]
     for p in procs:
         p.start()
     got = [q.get(timeout=600) for _ in procs]
@@ -65,9 +68,12 @@ def test_two_rank_render_equals_single_rank(precision, balance):
         assert p.exitcode == 0
     f, cam, cfg = _setup(precision)
     want = np.asarray(R.render_path(f, cam, cfg).data)
-    films = {r: np.frombuffer(b, dtype=want.dtype).reshape(want.shape) for r, b, _ in got}
-    assert np.array_equal(films[0], want) and np.array_equal(films[1], want)
-    assert sum(n for _, _, n in got) == W * H * cfg.spp
+    films = {r: b for r, b, _, _ in got}
+    assert films[1] is None
+    assert np.array_equal(np.frombuffer(films[0], dtype=want.dtype).reshape(want.shape), want)
+    assert sum(n for _, _, n, _ in got) == W * H * cfg.spp
+    if balance:   # the pilot ran on both ranks and reports its setup time
+        assert all(p is not None and p > 0 for _, _, _, p in got)
 
 
 def test_tile_owner_table_partitions_film_exactly():

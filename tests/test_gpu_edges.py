@@ -111,14 +111,80 @@ def test_from_checkpoint_and_bad_checkpoint(tmp_path, pair):
 
 
 def test_reference_render_modes_run_on_the_shim(pair, reference):
-    """The reference's own render_depth / render_normal / render_shaded run on
-    CudaNeuralField unchanged (protocol drop-in)."""
+    """The drop-in: the reference's own render_depth / render_normal /
+    render_shaded (render.py:144-184, host loop, backend protocol calls) run
+    on CudaNeuralField unchanged and equal the one-call device modes (depth
+    and normal bit for bit, shading to the last ulp of numpy's light dot)."""
     _, f, _ = pair
     _, _, render = reference
-    cam = render.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=16, height=12)
+    cam = render.Camera(position=(0.3, 0.5, 3.0), look_at=(0.0, 0.1, 0.0), vfov=np.pi / 4, width=41, height=27)
     for mode in ("depth", "normal", "shaded"):
-        fb = render.render(f, cam, render.RenderConfig(mode=mode))
-        assert fb.data.shape[:2] == (12, 16)
+        cfg = render.RenderConfig(mode=mode, background=(0.1, 0.2, 0.3), light_dir=np.array([0.3, -2.0, 1.1]),
+                                  albedo=0.6)
+        host = render.render(f, cam, cfg).data                # the reference's loop over the protocol
+        dev = R.render(f, cam, cfg).data                      # ddf_render_mode (the reference's Camera as-is)
+        assert host.shape == dev.shape
+        if mode == "shaded":
+            np.testing.assert_allclose(dev, host, rtol=0, atol=1e-15)
+        else:
+            assert np.array_equal(dev, host)
+
+
+def test_reference_render_path_runs_on_the_shim(pair, reference):
+    """render.render_path (render.py:198-247) of the unmodified reference on
+    CudaNeuralField (host loop: numpy camera rays, _hit_normals, _cosine_dirs,
+    one trace_batch / normal_batch call per stage) against the one-call device
+    wavefront.  Both draw the same PCG64 stream; they can differ only where
+    CUDA's f64 sin/cos/acos (1-2 ulp from libm) move a bounce direction."""
+    _, f, _ = pair
+    _, _, render = reference
+    cam = render.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=32, height=24)
+    cfg = render.RenderConfig(mode="path", spp=3, bounces=3, albedo=0.7, env_radiance=1.0, seed=42)
+    host = render.render(f, cam, cfg).data[:, :, 0]
+    dev = R.render(f, cam, cfg).data[:, :, 0]
+    d = np.abs(host - dev)
+    print(f"reference loop on the shim vs device wavefront: RMSE {np.sqrt(np.mean(d ** 2)):.3g}, "
+          f"pixels differing {np.mean(d > 1e-12):.2%}")
+    assert np.sqrt(np.mean(d ** 2)) <= 1e-3 and np.mean(d > 1e-12) <= 0.02
+
+
+def test_reference_image_writers_take_device_framebuffers(pair, reference, tmp_path):
+    """write_pfm / write_ppm and the bench harness stay the reference's
+    (render.py:266-303); they consume the device renders unchanged."""
+    _, f, _ = pair
+    _, _, render = reference
+    cam = render.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=8, height=6)
+    render.write_pfm(R.render(f, cam, render.RenderConfig(mode="depth")), tmp_path / "d.pfm")
+    render.write_ppm(R.render(f, cam, render.RenderConfig(mode="path", spp=1, bounces=1)), tmp_path / "p.ppm")
+    assert (tmp_path / "d.pfm").read_bytes().startswith(b"Pf\n8 6\n-1.0\n")
+    assert len((tmp_path / "p.ppm").read_bytes()) == len(b"P6\n8 6\n255\n") + 8 * 6 * 3
+    with pytest.raises(ValueError):
+        R.render(f, cam, R.RenderConfig(mode="bogus"))
+
+
+def test_sign_rule_raises_numeric_error(reference):
+    """render.py:137-139: a normal exactly perpendicular to its ray violates
+    n . d < 0.  A linear net pred = z + 0.5 has gradient (0, 0, 1); a camera
+    on the x axis with z up and an odd film height sends its centre row with
+    d_z = 0 exactly.  The device modes raise NumericError from the device
+    error word; the reference's own loop on the shim raises its own class."""
+    from paper_2306_16142_b200.errors import NumericError
+    from paper_2306_16142_b200.neural import MlpModel
+    v = np.array([[0.0, 0.0, 1.0, 0.0, 0.0]])
+    m = MlpModel((5, 1), [v], [np.array([1.0])], [np.array([0.5])])
+    f = CudaNeuralField(m, D, bounds=BOX)
+    cam = R.Camera(position=(3.0, 0.0, 0.0), look_at=(0.0, 0.0, 0.0), up=(0.0, 0.0, 1.0), vfov=np.pi / 4,
+                   width=9, height=7)
+    for mode in ("normal", "shaded"):
+        with pytest.raises(NumericError, match="sign rule"):
+            R.render(f, cam, R.RenderConfig(mode=mode))
+    assert np.all(np.isfinite(R.render(f, cam, R.RenderConfig(mode="depth")).data))
+    _, _, render = reference
+    rcam = render.Camera(position=(3.0, 0.0, 0.0), look_at=(0.0, 0.0, 0.0), up=(0.0, 0.0, 1.0), vfov=np.pi / 4,
+                         width=9, height=7)
+    from ddfield.errors import NumericError as RefNumericError
+    with pytest.raises(RefNumericError):
+        render.render(f, rcam, render.RenderConfig(mode="normal"))
 
 
 @pytest.mark.parametrize("mode", ["depth", "normal", "shaded", "ambient"])
@@ -133,19 +199,6 @@ def test_single_bounce_render_modes(pair, mode):
     fin = np.isfinite(ref)
     assert np.array_equal(fin, np.isfinite(img))
     assert np.max(np.abs(img[fin] - ref[fin])) <= 1e-3
-
-
-def test_image_writers_and_bench(tmp_path, pair):
-    _, f, _ = pair
-    cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=8, height=6)
-    R.write_pfm(R.render(f, cam, R.RenderConfig(mode="depth")), tmp_path / "d.pfm")
-    R.write_ppm(R.render(f, cam, R.RenderConfig(mode="path", spp=1, bounces=1)), tmp_path / "p.ppm")
-    assert (tmp_path / "d.pfm").read_bytes().startswith(b"Pf\n8 6\n-1.0\n")
-    assert len((tmp_path / "p.ppm").read_bytes()) == len(b"P6\n8 6\n255\n") + 8 * 6 * 3
-    rows = R.bench({"ddf": f}, cam, R.RenderConfig(mode="depth"), 3)
-    assert [r[3] for r in rows] == [1, 0, 0]
-    with pytest.raises(ValueError):
-        R.render(f, cam, R.RenderConfig(mode="bogus"))
 
 
 def test_config4_network_path_parity_fp32():
@@ -173,45 +226,24 @@ def test_config4_network_path_parity_fp32():
     assert np.mean(d > 1e-6) <= 0.25
 
 
-class _ProtocolOnly:
-    """Hides the device handle so render_* take the host protocol path
-    (pixel_rays on the host, trace_batch / normal_batch calls)."""
-
-    def __init__(self, f):
-        self._f = f
-
-    def trace_batch(self, o, d):
-        return self._f.trace_batch(o, d)
-
-    def trace_with_objects(self, o, d):
-        return self._f.trace_with_objects(o, d)
-
-    def normal_batch(self, o, d, t_hit=None, obj=None):
-        return self._f.normal_batch(o, d, t_hit=t_hit, obj=obj)
-
-
-@pytest.mark.parametrize("scene", [False, True])
-def test_device_render_modes_equal_protocol_path(scene):
-    """ddf_render_mode (everything on the device) == the host protocol path
-    on the same field: depth and normal bit for bit, shading to the last ulp
-    of the light dot product (numpy's matvec may fuse differently)."""
+def test_device_render_modes_scene_vs_oracle():
+    """Composite scene (config 5 layout): the device modes use the hit
+    object's gradient, as the oracle (and the reference subclass of
+    tests/golden/make_golden.py) does."""
     from paper_2306_16142_b200 import configs as C
-    if scene:
-        centers, scale, albedos = C.scene_layout()
-        ms = [kaiming_uniform((5, 32, 32, 1), s) for s in range(10, 18)]
-        f = CudaNeuralField.scene(ms, centers, scale, albedos, D, bounds=C.SCENE_BOX)
-    else:
-        f = CudaNeuralField(kaiming_uniform((65, 64, 64, 1), 4), D, bounds=BOX)
+    centers, scale, albedos = C.scene_layout()
+    ms = [kaiming_uniform((5, 32, 32, 1), s) for s in range(10, 18)]
+    f = CudaNeuralField.scene(ms, centers, scale, albedos, D, bounds=C.SCENE_BOX)
+    of = O.Field([O.Net(m.widths, m.v, m.g, m.b) for m in ms], D, bounds=C.SCENE_BOX, centers=centers,
+                 scale=scale, albedos=albedos)
     cam = R.Camera(position=(0.3, 0.5, 3.0), look_at=(0.0, 0.1, 0.0), vfov=np.pi / 4, width=41, height=27)
-    proto = _ProtocolOnly(f)
+    oc = O.Cam((0.3, 0.5, 3.0), (0.0, 0.1, 0.0), vfov=np.pi / 4, width=41, height=27)
     for mode in ("depth", "normal", "shaded"):
-        cfg = R.RenderConfig(mode=mode, background=(0.1, 0.2, 0.3), light_dir=np.array([0.3, -2.0, 1.1]), albedo=0.6)
-        a = R.render(f, cam, cfg).data
-        b = R.render(proto, cam, cfg).data
-        if mode == "shaded":
-            np.testing.assert_allclose(a, b, rtol=0, atol=1e-15)
-        else:
-            assert np.array_equal(a, b)
+        img = R.render(f, cam, R.RenderConfig(mode=mode)).data
+        ref = O.render_mode(of, oc, mode)
+        fin = np.isfinite(ref)
+        assert np.array_equal(fin, np.isfinite(img))
+        assert np.max(np.abs(img[fin] - ref[fin])) <= 1e-3
 
 
 def test_device_render_mode_degenerate_normals():
@@ -224,7 +256,8 @@ def test_device_render_mode_degenerate_normals():
     f = CudaNeuralField(m, D, bounds=BOX)
     cam = R.Camera(position=(0.0, 0.0, 3.0), look_at=(0.0, 0.0, 0.0), vfov=np.pi / 4, width=9, height=7)
     img = R.render(f, cam, R.RenderConfig(mode="normal")).data.reshape(-1, 3)
-    _, d = R.pixel_rays(cam)
+    _, d = O.camera_rays(O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=9, height=7),
+                         np.full((63, 2), 0.5), np.arange(63))
     o = np.broadcast_to(cam.position, d.shape)
     t, hit = f.trace_batch(o, d)
     assert hit.all()

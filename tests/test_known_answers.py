@@ -174,8 +174,8 @@ def test_oracle_normals_kappa_rule_and_finite_differences():
 
 
 def test_camera_centre_on_axis_corners_mirrored():
-    for cam in (R.Camera(position=(0.3, -0.2, 3.0), look_at=(0.1, 0.2, -0.4), vfov=np.pi / 4, width=33, height=21),):
-        o, d = R.pixel_rays(cam)
+    for cam in (O.Cam((0.3, -0.2, 3.0), (0.1, 0.2, -0.4), vfov=np.pi / 4, width=33, height=21),):
+        o, d = O.camera_rays(cam, np.full((33 * 21, 2), 0.5), np.arange(33 * 21))
         c = (cam.height // 2) * cam.width + cam.width // 2
         assert np.max(np.abs(d[c] - cam.forward)) < 1e-9
         W, H = cam.width, cam.height
@@ -287,7 +287,8 @@ def test_gpu_furnace_ambient_and_absorbing(cuda, prec):
     assert np.all(amb.data == 0.7 * 1.3) and np.all(fb.data == film_value(0.7 * 1.3, 8))
     np.testing.assert_allclose(amb.data, fb.data, rtol=1e-15)
     # depth: every pixel hits the top face at t_enter = (3 - 1) / |d_z|
-    o, d = R.pixel_rays(cam)
+    oc = O.Cam(cam.position, cam.look_at, vfov=cam.vfov, width=cam.width, height=cam.height)
+    o, d = O.camera_rays(oc, np.full((cam.width * cam.height, 2), 0.5), np.arange(cam.width * cam.height))
     depth = R.render_depth(f, cam).data.reshape(-1)
     np.testing.assert_allclose(depth, 2.0 / np.abs(d[:, 2]), rtol=1e-12)
     # zero-emission / all-absorbing -> black

@@ -146,3 +146,90 @@ def test_oracle_matches_live_reference(reference):
     assert np.array_equal(neural.forward_batch(m, x), O.mlp_forward(net, x))
     f = field.NeuralField(m, 2.0)  # default bounds
     assert np.array_equal(f.bounds, O.Field([net], 2.0).bounds)
+
+
+# ------------------------------------------------------------------ extensions
+# tests/golden/reference_golden_ext.npz comes from the reference with App. A's
+# subclasses layered on it (make_golden.py: EncodedNeuralField,
+# SceneNeuralField, render_path_ext): the reference still marches, takes
+# normals, samples bounces and builds camera rays.
+
+@pytest.fixture(scope="module")
+def ext():
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden_ext.npz"))
+
+
+def pe_field():
+    return O.Field([O.kaiming_uniform_net((65, 128, 128, 1), 6)], CFG_DELTA, bounds=BOX)
+
+
+def scene_field():
+    import itertools
+    centers = np.array(list(itertools.product((-0.75, 0.75), repeat=3)), dtype=np.float64)
+    albedos = np.random.default_rng(5).uniform(0.2, 0.9, 8)
+    nets = [O.kaiming_uniform_net((65, 32, 32, 1), s) for s in range(10, 18)]
+    return O.Field(nets, CFG_DELTA, bounds=np.array([[-1.25] * 3, [1.25] * 3]), centers=centers, scale=0.5,
+                   albedos=albedos)
+
+
+def test_pe_field_matches_encoded_reference(ext):
+    f = pe_field()
+    o, d = ext["pe_o"], ext["pe_d"]
+    ang = O.dirs_to_angles(d)
+    net = f.nets[0]
+    assert np.array_equal(O.mlp_forward(net, O.pe_encode(O.encode5(o, ang))), ext["pe_forward"])
+    assert np.array_equal(O.net_grad5(net, o, ang), ext["pe_grad5"])
+    t, h = f.query(o, d)
+    assert np.array_equal(t, ext["pe_query_t"]) and np.array_equal(h, ext["pe_query_hit"])
+    t, h, _ = f.trace(o * 2.5, d)
+    assert np.array_equal(t, ext["pe_trace_t"]) and np.array_equal(h, ext["pe_trace_hit"])
+    n, v = f.normal(o * 2.5, d, np.where(np.isfinite(t), t, 0.0))
+    assert np.array_equal(n, ext["pe_normal"]) and np.array_equal(v, ext["pe_normal_valid"])
+
+
+def test_pe_and_rr_renders_match_reference_loop(ext):
+    f = pe_field()
+    cam = O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=24, height=16)
+    v = O.render_path(f, cam, O.PathConfig(spp=2, bounces=2, albedo=0.7, env=1.0, seed=42))
+    assert np.array_equal(v.reshape(16, 24), ext["pe_film"])
+    v = O.render_path(f, cam, O.PathConfig(spp=3, bounces=6, albedo=0.7, env=1.0, seed=8, rr_start=1))
+    assert np.array_equal(v.reshape(16, 24), ext["pe_rr_film"])
+
+
+def test_scene_matches_reference_subclass(ext):
+    f = scene_field()
+    t, h, obj = f.trace(ext["sc_o"], ext["sc_d"])
+    assert np.array_equal(t, ext["sc_trace_t"]) and np.array_equal(h, ext["sc_trace_hit"])
+    assert np.array_equal(obj[h], ext["sc_trace_obj"][h])
+    n, v = f.normal(ext["sc_o"][h], ext["sc_d"][h], t[h], obj[h])
+    assert np.array_equal(n, ext["sc_normal"]) and np.array_equal(v, ext["sc_normal_valid"])
+    cam = O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=20, height=14)
+    for rr, key in ((-1, "sc_film"), (2, "sc_rr_film")):
+        v = O.render_path(f, cam, O.PathConfig(spp=2, bounces=4, albedo=0.7, env=1.0, seed=42, rr_start=rr))
+        assert np.array_equal(v.reshape(14, 20), ext[key])
+
+
+def test_render_stage_lists_match_reference_lengths():
+    """The oracle's per-stage lists have the lengths the unmodified
+    reference's render loop produced (make_golden.main_stages logs them from
+    a NeuralField subclass), stage by stage, for the config-2 render and the
+    march regime; each list is ascending (np.nonzero order)."""
+    st = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden_stages.npz"))
+    cases = [
+        (O.Field([O.kaiming_uniform_net((5,) + (256,) * 8 + (1,), 1)], CFG_DELTA, bounds=BOX), 128, 128,
+         O.PathConfig(spp=4, bounces=2, albedo=0.7, env=1.0, seed=42), "r2_stages", None),
+        (O.Field([march_net()], 0.1, bounds=BOX), 20, 12,
+         O.PathConfig(spp=3, bounces=3, albedo=0.6, env=1.5, seed=9), "rm_stages", None),
+        (O.Field([march_net()], 0.1, bounds=BOX), 48, 32,
+         O.PathConfig(spp=2, bounces=3, albedo=0.6, env=1.5, seed=9), "rmb_stages", "rmb_film"),
+    ]
+    for f, w, h, cfg, key, film in cases:
+        log = []
+        img = O.render_path(f, O.Cam((0.0, 0.0, 3.0), (0.0, 0.0, 0.0), vfov=np.pi / 4, width=w, height=h), cfg,
+                            log=log)
+        assert O.stage_sequence(log) == [tuple(r) for r in st[key].tolist()]
+        for rec in log:
+            for lst in rec["primary_march"] + rec["bounce_alive"] + [x for b in rec["bounce_march"] for x in b]:
+                assert np.all(np.diff(lst) > 0)
+        if film:
+            assert np.array_equal(img.reshape(h, w), st[film])
