@@ -65,8 +65,9 @@ def parse():
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16", "fp32_simt"])
     ap.add_argument("--cpu-baseline", type=int, default=1, help="time the oracle port on rank 0 at N=1")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--tile-balance", default="pilot", choices=["pilot", "rr"],
-                    help="N>1: tiles to ranks by a measured spp=1 pilot (LPT), or round-robin")
+    ap.add_argument("--tile-balance", default="rr", choices=["rr", "pilot"],
+                    help="N>1: 64x64 tiles round-robin (config 4's rule, default) or by a measured spp=1 pilot "
+                         "(LPT, every rank pilots its share)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank logic with several ranks on one GPU")
     return ap.parse_args()
@@ -114,9 +115,13 @@ def cpu_render_sample(name):
                        rr_start=w.get("rr_start", -1))
     t0 = time.perf_counter()
     n = 0
+    per_band = []
     for a, b in bands:
+        tb = time.perf_counter()
         O.render_path(fld, cam, cfg, pix_range=(a, b))
         n += (b - a) * spp
+        per_band.append((b - a) * spp / (time.perf_counter() - tb))
+    cpu_render_sample.band_rates = per_band
     return n, time.perf_counter() - t0
 
 
@@ -137,8 +142,12 @@ def cpu_baseline(name, runs=1):
     for _ in range(runs):
         n, s = cpu_render_sample(name)
         vals.append(n / s)
-    return {"value": statistics.median(vals), "unit": "path_samples/s", "cores": cpu_cores(), "kind": "port",
-            "sample": desc + "; float64 numpy oracle (oracle/cpu_ddf.py), OpenBLAS threads"}
+    out = {"value": statistics.median(vals), "unit": "path_samples/s", "cores": cpu_cores(), "kind": "port",
+           "sample": desc + "; float64 numpy oracle (oracle/cpu_ddf.py), OpenBLAS threads"}
+    rates = getattr(cpu_render_sample, "band_rates", [])
+    if len(rates) > 1:   # sampling error of the band sample: spread of the per-band rates
+        out["band_rate_rel_stderr"] = float(np.std(rates, ddof=1) / np.mean(rates) / np.sqrt(len(rates)))
+    return out
 
 
 # ----------------------------------------------------------------- config 1: query batch
@@ -716,21 +725,28 @@ def main():
     fld = C.build_field(name, precision=prec)
     cam = C.camera(name)
     cfg = C.render_config(name, rank=rank, world=world)
+    from paper_2306_16142_b200.dist import balanced_owners_distributed, reduce_film, render_path_distributed
+    pilot_s = None
     if world > 1 and args.tile_balance == "pilot":
-        # setup, outside the timed region: rank 0's spp=1 pilot costs every
-        # tile, the LPT table is broadcast (dist.balanced_owners_distributed)
-        from paper_2306_16142_b200.dist import balanced_owners_distributed
-        cfg.tile_owner = balanced_owners_distributed(fld, cam, cfg, world, tile=cfg.tile)
+        # setup, outside the timed region: every rank pilots its round-robin
+        # share of the tiles at spp = 1, one exact sum of the cost vector, the
+        # same LPT table on every rank (dist.balanced_owners_distributed)
+        cfg.tile_owner, secs = balanced_owners_distributed(fld, cam, cfg, world)
+        t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        pilot_s = float(t.item())
     n_pix = cam.width * cam.height
     accum = torch.empty(n_pix, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
     def step(profile=0):
+        """One render of this rank's tiles plus the one collective: the film
+        summed onto rank 0 (exact: every pixel has one non-zero term)."""
         cfg.profile = profile
         _, st = R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
         if world > 1:
-            dist.all_reduce(accum, op=dist.ReduceOp.SUM)
+            reduce_film(accum)
         return st
 
     for _ in range(max(3, args.warmup)):
@@ -830,6 +846,34 @@ def main():
         roofline["compaction"] = {"bound": "hbm", "ms": stp["ms_compact"], "bytes": cbytes, "achieved": gbps,
                                   "peak": hbm, "unit": "GB/s", "frac": gbps / hbm,
                                   "calls_per_wave": calls, "note": "launch-latency bound below ~8 M slots per call"}
+    # the wavefront kernels against HBM: algorithmic bytes are
+    # the path-state fields each kernel must read and write (structure of
+    # arrays, f64; wavefront.cuh), minimum counts where a write depends on
+    # the path's outcome
+    P = samples
+    alive_rows = int(sum(stp["bounce_alive_rows"]))
+    rr_b = max(0, cfg.bounces - cfg.rr_start) if cfg.rr_start >= 0 else 0
+    own = n_pix if world == 1 else int(stp["path_samples"]) // cfg.spp
+    wave_bytes = {
+        # pix 4 | o, d 48 | thr, rad 16 | alive 1 | u34 16 | t_acc, t_exit, t 24 | march, hit, gdone 3 | obj 4
+        "camera_kernel": ("ms_camera", 116 * P, "per slot: pixel id in; o, d, throughput, radiance, trace state out"),
+        # per slot: hit in, alive out; per bounce-alive row: list entry + hit in
+        "after_kernels": ("ms_after", 2 * P + 5 * alive_rows, "after_primary (hit -> alive) + after_bounce (list, hit)"),
+        # per slot and RR bounce: alive in; per surviving row: pixel id + throughput in, throughput out
+        "roulette_kernel": ("ms_roulette", rr_b * P + 20 * alive_rows if rr_b else 0, "alive flags, survivors' throughput"),
+        # per alive row: list 4 | o, d, g3 72 | t 8 | obj 4 | thr 8 | pix 4 in; thr 8 | o, d 48 | trace state 47 | want 1 out
+        "bounce_kernel": ("ms_bounce", 204 * alive_rows, "normal, hit point, cosine bounce, slab test"),
+        # per owned pixel: id 4, accumulator 8 in and out; per slot: radiance 8
+        "film_kernel": ("ms_film", 20 * own * stp["waves"] + 8 * P, "accum += radiance in spp order"),
+    }
+    wf = {}
+    for kname, (key, nbytes, what) in wave_bytes.items():
+        t_ms = stp.get(key) or 0.0
+        if t_ms > 0 and nbytes > 0:
+            gbps = nbytes / (t_ms / 1e3) / 1e9
+            wf[kname] = {"ms": t_ms, "bytes": int(nbytes), "achieved": gbps, "frac": gbps / hbm, "what": what}
+    roofline["wavefront"] = {"bound": "hbm", "peak": hbm, "unit": "GB/s", "kernels": wf}
+
     # DRAM traffic per launch of the dominant kernel from the committed ncu
     # --set full capture of this workload (profiles/), next to the
     # algorithmic path-state bytes of that launch
@@ -854,7 +898,10 @@ def main():
         except Exception:
             pass
 
-    # end to end through the public API: host film out, RNG tables in
+    # end to end through the public API (render.render_path at N = 1,
+    # dist.render_path_distributed at N > 1): each call allocates its own
+    # accumulator, uploads the PCG64 jump tables and returns the (H, W, 3)
+    # film on the host (rank 0)
     e2e = None
     if not args.no_e2e:
         ts = []
@@ -863,11 +910,10 @@ def main():
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            acc, _ = R.render_path_device(fld, cam, cfg, accum=accum, stream=stream)
             if world > 1:
-                dist.reduce(acc, dst=0, op=dist.ReduceOp.SUM)
-            if rank == 0:
-                R.film_from_accum(acc, cam, cfg.spp)
+                render_path_distributed(fld, cam, cfg, tile_owner=cfg.tile_owner)
+            else:
+                R.render_path(fld, cam, cfg)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
         te = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device="cuda")
@@ -875,7 +921,8 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": samples_total / te.item(), "unit": "path_samples/s",
                "h2d_bytes_per_step": 2 * (16 + 64 * 32) + 0,   # PCG64 jump tables (camera/config are kernel params)
-               "d2h_bytes_per_step": n_pix * 8 + 160}
+               "d2h_bytes_per_step": n_pix * 8 + 160,
+               "api": "render.render_path" if world == 1 else "dist.render_path_distributed"}
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_baseline:
@@ -891,6 +938,7 @@ def main():
                        "tiles": cfg.tile, "parallelism": f"tiles{world}" if world > 1 else "single",
                        "tile_assignment": (("pilot-balanced (LPT)" if cfg.tile_owner is not None else "round-robin")
                                            if world > 1 else None),
+                       "collective": "film sum-reduce to rank 0 (NCCL), inside the step" if world > 1 else None,
                        "l2": "flushed (256 MB write) between timed steps"},
             "ddf_queries_per_s": stp["forward_rows"] / (ms / 1e3),
             "gradient_rows_per_s": stp["gradient_rows"] / (ms / 1e3),
@@ -899,6 +947,8 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
         }
+        if pilot_s is not None:
+            out["pilot_setup_s"] = pilot_s
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -77,7 +77,9 @@ typedef struct {
   /* 1: time every kernel class with CUDA events on `stream` (stats.ms_*) */
   int32_t profile;
   /* 1: replay the waves as a CUDA graph captured on the first call with the
-     same camera, config, accumulator and field (ignored when profile = 1) */
+     same camera, config and field (ignored when profile = 1 or stage_log is
+     set).  The graph renders into the field's own film buffer, copied to
+     accum at the end, so the caller's accumulator may move between calls. */
   int32_t graph;
   /* 1: never fuse a bounce ray's first march step with the next bounce's
      normal gradient (0 = fuse where the engine and regime allow; results
@@ -139,6 +141,11 @@ typedef struct {
   uint64_t primary_march_rows[DDF_STAGE_STEPS];
   uint64_t bounce_alive_rows[DDF_STAGE_BOUNCES];
   uint64_t bounce_march_rows[DDF_STAGE_BOUNCES];
+  /* profile = 1 only: the wavefront kernels of ms_other one by one
+     (camera_kernel; roulette_kernel; bounce_kernel; after_primary_kernel +
+     after_bounce_kernel; film_kernel) for their HBM roofline */
+  double ms_camera, ms_roulette, ms_bounce, ms_after, ms_film;
+  int32_t graph_replayed;  /* 1: this call replayed a captured CUDA graph     */
 } ddf_render_stats_t;
 
 /* NeuralField.__init__ (field.py:231-237): delta, AABB bounds (lo xyz, hi xyz). */

@@ -91,7 +91,9 @@ class RenderStats_t(ctypes.Structure):
                 ("fused_launches", ctypes.c_uint64), ("ms_fused", ctypes.c_double),
                 ("primary_march_rows", ctypes.c_uint64 * STAGE_STEPS),
                 ("bounce_alive_rows", ctypes.c_uint64 * STAGE_BOUNCES),
-                ("bounce_march_rows", ctypes.c_uint64 * STAGE_BOUNCES)]
+                ("bounce_march_rows", ctypes.c_uint64 * STAGE_BOUNCES),
+                ("ms_camera", ctypes.c_double), ("ms_roulette", ctypes.c_double), ("ms_bounce", ctypes.c_double),
+                ("ms_after", ctypes.c_double), ("ms_film", ctypes.c_double), ("graph_replayed", ctypes.c_int32)]
 
 
 def stats_dict(st: RenderStats_t) -> dict:

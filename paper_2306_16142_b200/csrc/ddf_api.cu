@@ -64,7 +64,9 @@ struct Buf {
 
 // Per-call kernel-class timing (cfg->profile) and launch counting.
 struct Prof {
-  enum { FWD = 0, GRAD = 1, COMPACT = 2, OTHER = 3, TOTAL = 4, FUSED = 5, NCAT = 6 };
+  // OTHER = the wavefront kernels, split per kernel for the HBM roofline
+  enum { FWD = 0, GRAD = 1, COMPACT = 2, OTHER = 3, TOTAL = 4, FUSED = 5, CAMERA = 6, ROULETTE = 7, BOUNCE = 8,
+         AFTER = 9, FILM = 10, NCAT = 11 };
   bool on = false;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
@@ -109,6 +111,7 @@ struct ddf_field_s {
   Buf t_acc, t_exit, alive, list, list2, blocks, small, ones;
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
   Buf pix, rng, umma_masks, st_u34, st_g3, st_gdone, st_want;
+  Buf film;   // the render's accumulator: captured graphs write here, the caller's buffer gets a copy
   Buf udf_dirs, udf_vals, udf_pts, udf_best, udf_arg, udf_found, udf_list, udf_seg, udf_state;
   // captured render_path waves (cfg->graph): replayed while the key matches
   unsigned long long gen = 0;            // bumped by add_network / set_precision
@@ -917,9 +920,9 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     f->pix_n = (int)own.size();
   }
   const int n_own = f->pix_n;
-  CUDA_TRY(cudaMemsetAsync(accum, 0, sizeof(double) * n_pix, st));
   CUDA_TRY(cudaMemsetAsync(f->small.p, 0, 4096, st));
   if (n_own == 0) {
+    CUDA_TRY(cudaMemsetAsync(accum, 0, sizeof(double) * n_pix, st));
     if (stats) std::memset(stats, 0, sizeof(*stats));
     f->prof.reset(false);
     return DDF_OK;
@@ -955,6 +958,9 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
   CUDA_TRY(f->st_want.ensure(P));
   CUDA_TRY(f->list.ensure(sizeof(int) * P));
   CUDA_TRY(f->list2.ensure(sizeof(int) * P));
+  CUDA_TRY(f->film.ensure(sizeof(double) * n_pix));
+  double* film = f->film.as<double>();
+  CUDA_TRY(cudaMemsetAsync(film, 0, sizeof(double) * n_pix, st));
 
   PathState S{};
   S.o = f->st_o.as<double>(); S.d = f->st_d.as<double>();
@@ -1004,7 +1010,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
       const int Pw = w.ns * n_own;
       const int g = (Pw + 255) / 256;
       {
-        ProfScope ps(f->prof, Prof::OTHER, ss);
+        ProfScope ps(f->prof, Prof::CAMERA, ss);
         camera_kernel<<<g, 256, 0, ss>>>(f->F, C, w, S, Pw);
         f->prof.launches += 1;
       }
@@ -1019,13 +1025,13 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
         return rc;
       }
       {
-        ProfScope ps(f->prof, Prof::OTHER, ss);
+        ProfScope ps(f->prof, Prof::AFTER, ss);
         after_primary_kernel<<<g, 256, 0, ss>>>(w, S, Pw);
         f->prof.launches += 1;
       }
       for (int b = 0; b < cfg->bounces; ++b) {
         if (cfg->rr_start >= 0 && b >= cfg->rr_start) {
-          ProfScope ps(f->prof, Prof::OTHER, ss);
+          ProfScope ps(f->prof, Prof::ROULETTE, ss);
           roulette_kernel<<<g, 256, 0, ss>>>(w, S, Pw, b);
           f->prof.launches += 1;
         }
@@ -1056,7 +1062,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
           if ((rc = run_mlp(f, f->F, op, Pw, true, ss))) return rc;
         }
         {
-          ProfScope ps(f->prof, Prof::OTHER, ss);
+          ProfScope ps(f->prof, Prof::BOUNCE, ss);
           bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(f->F_dev, w, S, f->list.as<int>(), sm.count2, b);
           f->prof.launches += 1;
         }
@@ -1073,14 +1079,14 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
           return rc;
         }
         {
-          ProfScope ps(f->prof, Prof::OTHER, ss);
+          ProfScope ps(f->prof, Prof::AFTER, ss);
           after_bounce_kernel<<<std::min(g, f->sm_count * 8), 256, 0, ss>>>(w, S, f->list.as<int>(), sm.count2);
           f->prof.launches += 1;
         }
       }
       {
-        ProfScope ps(f->prof, Prof::OTHER, ss);
-        film_kernel<<<(n_own + 255) / 256, 256, 0, ss>>>(w, S, accum);
+        ProfScope ps(f->prof, Prof::FILM, ss);
+        film_kernel<<<(n_own + 255) / 256, 256, 0, ss>>>(w, S, film);
         f->prof.launches += 1;
       }
       CUDA_TRY(cudaGetLastError());
@@ -1089,7 +1095,8 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     return DDF_OK;
   };
   // CUDA graph replay (cfg->graph): the captured loop is keyed by the field
-  // generation, the buffer epoch, the camera, the config and the accumulator
+  // generation, the buffer epoch, the camera and the config.  It writes the
+  // field's own film buffer, so any caller accumulator can replay it.
   const bool use_graph = cfg->graph != 0 && !f->prof.on && !lg_on;
   std::vector<unsigned char> gkey;
   if (use_graph) {
@@ -1097,14 +1104,12 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     kc.profile = 0;
     kc.graph = 0;
     const unsigned long long gen = f->gen;
-    const void* acc = accum;
     auto put = [&](const void* p, size_t n) { gkey.insert(gkey.end(), (const unsigned char*)p, (const unsigned char*)p + n); };
     put(&gen, sizeof gen);
     put(cam, sizeof(*cam));
     kc.tile_owner = nullptr;   // the table's contents, not its address, key the graph
     kc.stage_log = nullptr;
     put(&kc, sizeof kc);
-    put(&acc, sizeof acc);
     if (!owner.empty()) put(owner.data(), sizeof(int32_t) * owner.size());
   }
   auto epoch_key = [&]() {
@@ -1112,8 +1117,10 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     k.insert(k.end(), (const unsigned char*)&g_buf_epoch, (const unsigned char*)&g_buf_epoch + sizeof g_buf_epoch);
     return k;
   };
+  bool replayed = false;
   if (use_graph && f->graph_exec && f->graph_key == epoch_key()) {
     CUDA_TRY(cudaGraphLaunch(f->graph_exec, st));
+    replayed = true;
     waves = f->graph_waves;
     f->prof.launches = f->graph_launches[0];
     f->prof.fwd_launches = f->graph_launches[1];
@@ -1150,6 +1157,7 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
       waves = w0;
     }
   }
+  CUDA_TRY(cudaMemcpyAsync(accum, film, sizeof(double) * n_pix, cudaMemcpyDeviceToDevice, st));
   if (f->prof.on) f->prof.marks[Prof::TOTAL].push_back({t_begin, f->prof.rec(st)});
   int host_small[32 + 2 * SMALL_U64];
   CUDA_TRY(cudaMemcpyAsync(host_small, f->small.p, sizeof(host_small), cudaMemcpyDeviceToHost, st));
@@ -1171,7 +1179,14 @@ int ddf_render_path(ddf_field_t f, const ddf_camera_t* cam, const ddf_path_confi
     stats->ms_forward = f->prof.total_ms(Prof::FWD);
     stats->ms_gradient = f->prof.total_ms(Prof::GRAD);
     stats->ms_compact = f->prof.total_ms(Prof::COMPACT);
-    stats->ms_other = f->prof.total_ms(Prof::OTHER);
+    stats->graph_replayed = replayed ? 1 : 0;
+    stats->ms_camera = f->prof.total_ms(Prof::CAMERA);
+    stats->ms_roulette = f->prof.total_ms(Prof::ROULETTE);
+    stats->ms_bounce = f->prof.total_ms(Prof::BOUNCE);
+    stats->ms_after = f->prof.total_ms(Prof::AFTER);
+    stats->ms_film = f->prof.total_ms(Prof::FILM);
+    stats->ms_other = f->prof.total_ms(Prof::OTHER) + stats->ms_camera + stats->ms_roulette + stats->ms_bounce +
+                      stats->ms_after + stats->ms_film;
     stats->ms_total = f->prof.total_ms(Prof::TOTAL);
     for (int j = 0; j < DDF_STAGE_STEPS; ++j) stats->primary_march_rows[j] = hs64[16 + j];
     for (int b = 0; b < DDF_STAGE_BOUNCES; ++b) {

@@ -265,7 +265,7 @@ def test_device_render_mode_degenerate_normals():
 
 
 def test_graph_replay_identical_and_invalidated():
-    """cfg.graph: the second call with the same camera / config / accumulator
+    """cfg.graph: the second call with the same camera / config
     replays the captured waves.  Replays equal eager renders; a precision
     change (field generation) or a scratch reallocation by another call
     (buffer epoch) forces a fresh capture instead of a stale replay."""
@@ -286,3 +286,11 @@ def test_graph_replay_identical_and_invalidated():
     f.trace_batch(big * 2.5, dirs)                       # grows (reallocates) the shared scratch
     assert torch.equal(R.render_path_device(f, cam, cfg, accum=acc)[0], bf)
     assert torch.equal(R.render_path_device(f, cam, cfg, accum=acc)[0], bf)
+    # the graph renders into the field's own film: a new accumulator per call
+    # (what the public render_path does) replays the same graph
+    launches = R.render_path_device(f, cam, cfg)[1]["kernel_launches"]
+    for _ in range(2):
+        other = torch.full((48 * 32,), 7.0, dtype=torch.float64, device="cuda")
+        got, st = R.render_path_device(f, cam, cfg, accum=other)
+        assert torch.equal(got, bf) and st["kernel_launches"] == launches and st["graph_replayed"] == 1
+    assert np.array_equal(R.render_path(f, cam, cfg).data[:, :, 0].reshape(-1), bf.cpu().numpy() / 3)

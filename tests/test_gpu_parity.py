@@ -92,7 +92,8 @@ def test_trace_batch(golden, cfg1):
 def test_trace_multistep_march(golden):
     f = CudaNeuralField(as_model(march_net()), 0.1, bounds=BOX)
     t, hit = f.trace_batch(golden["m_origins"], golden["m_dirs"])
-    assert (hit == golden["m_trace_hit"]).mean() >= 0.99
+    print(f"march regime trace: hit agreement {(hit == golden['m_trace_hit']).mean():.4f}")
+    assert (hit == golden["m_trace_hit"]).mean() >= 0.999
     both = hit & golden["m_trace_hit"]
     assert np.max(np.abs(t[both] - golden["m_trace_t"][both])) <= 1e-4
 
@@ -190,7 +191,9 @@ def test_render_march_regime(golden):
     cfg = R.RenderConfig(mode="path", spp=3, bounces=3, albedo=0.6, env_radiance=1.5, seed=9)
     img = R.render_path(f, _cam(20, 12), cfg).data[:, :, 0]
     ref = golden["rm_film"]
-    assert np.sqrt(np.mean((img - ref) ** 2)) <= 3e-2
+    rmse = np.sqrt(np.mean((img - ref) ** 2))
+    print(f"march regime film vs reference: RMSE {rmse:.3g}")
+    assert rmse <= 3e-3
 
 
 def test_render_matches_oracle_small_with_waves():
