@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("DDF_B200_LIB") or os.path.join(LIB_DIR, "libddf_b200.
 HEADER = os.path.join(ROOT, "include", "ddf_b200.h")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+              "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+OBJ_DIR = os.path.join(HERE, "build")
 
 DDF_OK, DDF_EUSAGE, DDF_EDATA, DDF_ENUMERIC, DDF_ECUDA = 0, 1, 2, 3, 4
 PREC_FP32, PREC_BF16, PREC_FP32_SIMT = 0, 1, 2
@@ -37,21 +38,44 @@ EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "dd
 
 
 def build(verbose: bool = False, force: bool = False) -> str:
-    """Compile the CUDA sources into the in-tree shared library."""
-    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))]
-    if not force and os.path.exists(LIB_PATH):
-        newest = max(os.path.getmtime(p) for p in srcs + [HEADER])
-        if os.path.getmtime(LIB_PATH) >= newest:
-            return LIB_PATH
+    """Compile the CUDA sources into the in-tree shared library: every
+    translation unit (ddf_api.cu and the engine units eng_*.cu) in parallel
+    to build/*.o, then one nvcc link.  A unit is recompiled when it or any
+    header is newer than its object."""
+    units = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")] + [HEADER]
+    newest_header = max(os.path.getmtime(p) for p in headers)
+    os.makedirs(OBJ_DIR, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
+    extra = os.environ.get("DDF_NVCC_EXTRA", "").split()
+    objs, jobs = [], []
+    for u in units:
+        src = os.path.join(CSRC, u)
+        obj = os.path.join(OBJ_DIR, u[:-3] + ".o")
+        objs.append(obj)
+        stale = force or not os.path.exists(obj) or os.path.getmtime(obj) < max(newest_header, os.path.getmtime(src))
+        if stale:
+            cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", src, "-o", obj + ".tmp"]
+            jobs.append((obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    errors = []
+    for obj, proc in jobs:
+        out, _ = proc.communicate()
+        if proc.returncode != 0:
+            errors.append(out)
+        else:
+            os.replace(obj + ".tmp", obj)
+            if verbose and out:
+                print(out)
+    if errors:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(errors))
+    if not jobs and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(o) for o in objs):
+        return LIB_PATH
     tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, os.path.join(CSRC, "ddf_api.cu"), "-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    res = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp],
+                         capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    if verbose:
-        print(res.stdout + res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -8,6 +8,7 @@
 
 #include "../../include/ddf_b200.h"
 #include "compact.cuh"
+#include "engines.h"
 #include "ddf_common.cuh"
 #include "field_kernels.cuh"
 #include "mlp_umma.cuh"
@@ -162,26 +163,6 @@ int max_width(const FieldDev& F) {
 }
 
 // ---------------------------------------------------------------- engine dispatch
-template <int M, int KMAX>
-size_t simt_smem() {
-  return sizeof(double) * M * 8 + sizeof(float) * (2 * KMAX * M + 2 * simt::KC * simt::NC + 2 * M) +
-         sizeof(uint32_t) * DDF_MAX_LAYERS * KMAX * (M / 32) + sizeof(int) * 2 * M;
-}
-
-template <class Op, int M, int KMAX>
-int launch_simt(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool grad, cudaStream_t st) {
-  const size_t sm = simt_smem<M, KMAX>();
-  void (*kern)(const FieldDev, const Op);
-  if constexpr (Op::kGrad) kern = simt::grad_kernel<M, KMAX, Op>;
-  else kern = simt::forward_kernel<M, KMAX, Op>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  int tiles = (max_rows + M - 1) / M + (grad ? F.n_obj : 0);
-  int grid = std::max(1, std::min(tiles, f->sm_count));
-  kern<<<grid, simt::NT, sm, st>>>(F, op);
-  CUDA_TRY(cudaGetLastError());
-  return DDF_OK;
-}
-
 // RAII marker: records start/stop events of one kernel-class region
 struct ProfScope {
   Prof& p; int cat; cudaStream_t st; size_t a = 0;
@@ -207,7 +188,7 @@ int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool 
     } else {
       imgs = f->images_x3;
     }
-    int rc = x3::launch<Op>(F, imgs, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st, &g_err);
+    int rc = engines::x3_launch<Op>(F, imgs, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st, &g_err);
     return rc ? (rc == 1 ? DDF_EUSAGE : DDF_ECUDA) : DDF_OK;
   }
   bool tensor = F.precision == PREC_BF16;
@@ -222,13 +203,11 @@ int run_mlp(ddf_field_s* f, const FieldDev& F, const Op& op, int max_rows, bool 
     } else {
       imgs = f->images;
     }
-    int rc = umma::launch<Op>(F, imgs, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st, &g_err);
+    int rc = engines::umma_launch<Op>(F, imgs, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st, &g_err);
     return rc ? (rc == 1 ? DDF_EUSAGE : DDF_ECUDA) : DDF_OK;
   }
-  const int w = max_width(F);
-  if (w <= 256) return launch_simt<Op, 64, 256>(f, F, op, max_rows, grad, st);
-  if (w <= 512) return launch_simt<Op, 32, 512>(f, F, op, max_rows, grad, st);
-  return fail(DDF_EUSAGE, "fp32 engine supports layer widths up to 512");
+  const int rc = engines::simt_launch<Op>(F, op, max_rows, max_width(F), f->sm_count, st, &g_err);
+  return rc ? (rc == 1 ? DDF_EUSAGE : DDF_ECUDA) : DDF_OK;
 }
 
 // Fused trace step + input gradient (TraceGradOp, wavefront.cuh) on the
@@ -250,7 +229,7 @@ int run_fused(ddf_field_s* f, const TraceGradOp& op, int max_rows, cudaStream_t 
   f->prof.launches += 1;
   f->prof.fused_launches += 1;
   CUDA_TRY(f->umma_masks.ensure(sizeof(uint32_t) * (size_t)umma::MASK_WORDS_PER_CTA * umma::QS * f->sm_count));
-  int rc = umma::launch<TraceGradOp>(f->F, f->images, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st,
+  int rc = engines::umma_launch<TraceGradOp>(f->F, f->images, op, max_rows, f->sm_count, f->umma_masks.as<uint32_t>(), st,
                                      &g_err);
   return rc ? (rc == 1 ? DDF_EUSAGE : DDF_ECUDA) : DDF_OK;
 }
@@ -1305,12 +1284,8 @@ int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64
 
 int ddf_debug_counters(uint64_t* out16, int32_t reset) {
   unsigned long long h[16];
-  CUDA_TRY(cudaMemcpyFromSymbol(h, umma::g_dbg, sizeof(h)));
+  engines::umma_debug_counters(h, reset != 0);
   for (int i = 0; i < 16; ++i) out16[i] = h[i];
-  if (reset) {
-    std::memset(h, 0, sizeof(h));
-    CUDA_TRY(cudaMemcpyToSymbol(umma::g_dbg, h, sizeof(h)));
-  }
   return DDF_OK;
 }
 

@@ -49,7 +49,7 @@ inline int debug_bits() {
   static const int raw = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
   return kStats ? raw : (raw & ~kUnsafeDbg);
 }
-__device__ unsigned long long g_dbg[16];
+static __device__ unsigned long long g_dbg[16];   // per translation unit (engines.h sums them)
 #define DDF_DBG_T0() long long _t0 = kStats ? clock64() : 0
 #define DDF_DBG_ADD(i) do { if (kStats) dbg_acc[i] += (unsigned long long)(clock64() - _t0); } while (0)
 #define DDF_DBG_FLUSH() do { if (kStats) for (int _i = 0; _i < 16; ++_i) if (dbg_acc[_i]) atomicAdd(&g_dbg[_i], dbg_acc[_i]); } while (0)

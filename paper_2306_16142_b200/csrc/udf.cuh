@@ -34,10 +34,12 @@ __device__ __forceinline__ void query_u34(d3 d, double& u3, double& u4) {
 }
 
 // the encoded angles of a direction do not depend on the point: once per direction
+#ifndef DDF_OPS_ONLY
 __global__ void dir_u34_kernel(const double* dirs, int n, double* u34) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) query_u34(ld3(dirs, k), u34[2 * k], u34[2 * k + 1]);
 }
+#endif
 
 struct ScanOp : ListBase {
   static constexpr bool kGrad = false;
@@ -83,6 +85,7 @@ struct ProbeOp : ListBase {   // rows 2q + e: probe x1 (e = 0) or x2 (e = 1) of 
 };
 
 // one warp per point: first argmin over its n_dirs values (field.py:438-448)
+#ifndef DDF_OPS_ONLY
 __global__ void reduce_kernel(const double* vals, int n_pts, int n_dirs, double* best, int* arg, uint8_t* found) {
   const int lane = threadIdx.x & 31;
   const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -105,8 +108,10 @@ __global__ void reduce_kernel(const double* vals, int n_pts, int n_dirs, double*
     found[p] = bv < INF;
   }
 }
+#endif
 
 // found point q: start angles = vecs_to_angles(best direction) (field.py:449)
+#ifndef DDF_OPS_ONLY
 __global__ void polish_init(Polish P, const int* arg, const double* best, const double* dirs, int nq_max,
                             const int* nq) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -118,8 +123,10 @@ __global__ void polish_init(Polish P, const int* arg, const double* best, const 
   P.ang[2 * q + 1] = a1;
   P.val[q] = best[p];
 }
+#endif
 
 // field.py:462-470: window about the current angle, first probe pair
+#ifndef DDF_OPS_ONLY
 __global__ void gs_begin(Polish P, int axis, double half, double golden, int nq_max, const int* nq) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq_max || q >= *nq) return;
@@ -134,8 +141,10 @@ __global__ void gs_begin(Polish P, int axis, double half, double golden, int nq_
   P.x1[q] = dsub(b, dmul(golden, dsub(b, a)));
   P.x2[q] = dadd(a, dmul(golden, dsub(b, a)));
 }
+#endif
 
 // field.py:477-482: keep the side holding the smaller probe, new probe pair
+#ifndef DDF_OPS_ONLY
 __global__ void gs_step(Polish P, double golden, int nq_max, const int* nq) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq_max || q >= *nq) return;
@@ -146,8 +155,10 @@ __global__ void gs_step(Polish P, double golden, int nq_max, const int* nq) {
   P.x1[q] = dsub(b, dmul(golden, dsub(b, a)));
   P.x2[q] = dadd(a, dmul(golden, dsub(b, a)));
 }
+#endif
 
 // field.py:483-487: accept the better probe if it improves strictly
+#ifndef DDF_OPS_ONLY
 __global__ void gs_end(Polish P, int axis, int nq_max, const int* nq) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq_max || q >= *nq) return;
@@ -159,15 +170,19 @@ __global__ void gs_end(Polish P, int axis, int nq_max, const int* nq) {
     P.ang[2 * q + axis] = xs;
   }
 }
+#endif
 
+#ifndef DDF_OPS_ONLY
 __global__ void polish_scatter(Polish P, double* out, int nq_max, const int* nq) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq_max || q >= *nq) return;
   out[P.pidx[q]] = P.val[q];
 }
+#endif
 
 // recon.py:53-58: np.linspace(lo, hi, res) per axis (i * step + lo, last = hi),
 // ij meshgrid, C order (z fastest)
+#ifndef DDF_OPS_ONLY
 __global__ void grid_points_kernel(double* pts, int res, double lx, double ly, double lz, double hx, double hy,
                                    double hz) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -181,6 +196,7 @@ __global__ void grid_points_kernel(double* pts, int res, double lx, double ly, d
     pts[3 * i + k] = idx[k] == res - 1 ? hi[k] : dadd(dmul((double)idx[k], step), lo[k]);
   }
 }
+#endif
 
 }  // namespace udf
 }  // namespace ddf

@@ -77,6 +77,7 @@ __device__ __forceinline__ void begin_trace(const FieldDev& F, const PathState& 
 }
 
 // primary rays: render.py:213-220 + pixel_rays render.py:54-75
+#ifndef DDF_OPS_ONLY
 __global__ void camera_kernel(const FieldDev F, const CamDev C, const WaveDev w, const PathState S, int P) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
@@ -100,9 +101,11 @@ __global__ void camera_kernel(const FieldDev F, const CamDev C, const WaveDev w,
   S.alive[p] = 0;
   begin_trace(F, S, p, o, d);
 }
+#endif
 
 // render.py:54-75 pixel_rays at pixel centres (offsets 0.5) for the
 // single-bounce modes; slot p = pixel p
+#ifndef DDF_OPS_ONLY
 __global__ void camera_center_kernel(const FieldDev F, const CamDev C, const PathState S, int P) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
@@ -119,6 +122,7 @@ __global__ void camera_center_kernel(const FieldDev F, const CamDev C, const Pat
   st3(S.d, p, d);
   begin_trace(F, S, p, o, d);
 }
+#endif
 
 struct ModeDev {
   int mode, ambient;
@@ -127,6 +131,7 @@ struct ModeDev {
 
 // render.py:144-184 per pixel from the trace (t, hit) and, for hit pixels,
 // the spatial gradient / face cross product in g3 (_hit_normals semantics)
+#ifndef DDF_OPS_ONLY
 __global__ void mode_shade_kernel(const ModeDev m, const PathState S, int P, double* out, int* err,
                                   unsigned long long* degenerate) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -164,8 +169,10 @@ __global__ void mode_shade_kernel(const ModeDev m, const PathState S, int P, dou
   out[3 * (int64_t)p + 1] = rgb[1];
   out[3 * (int64_t)p + 2] = rgb[2];
 }
+#endif
 
 // render.py:218-219  escape of primary rays, alive = hit
+#ifndef DDF_OPS_ONLY
 __global__ void after_primary_kernel(const WaveDev w, const PathState S, int P) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
@@ -173,6 +180,7 @@ __global__ void after_primary_kernel(const WaveDev w, const PathState S, int P) 
   if (!h) S.rad[p] = w.env;
   S.alive[p] = h;
 }
+#endif
 
 // EXTENSION (config 4): Russian roulette at bounce b >= rr_start,
 // survival p = min(1, throughput), survivors divide by p.
@@ -181,6 +189,7 @@ __device__ __forceinline__ bool rr_survives(const WaveDev& w, double thr, int s,
   const double u = pcg_single(*w.rr, (uint64_t)(s * w.bounces + b) * (uint64_t)w.n_pix + (uint64_t)i);
   return u < q;
 }
+#ifndef DDF_OPS_ONLY
 __global__ void roulette_kernel(const WaveDev w, const PathState S, int P, int b) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P || !S.alive[p]) return;
@@ -190,6 +199,7 @@ __global__ void roulette_kernel(const WaveDev w, const PathState S, int P, int b
   if (rr_survives(w, S.thr[p], s, i, b, q)) S.thr[p] = ddiv(S.thr[p], q);
   else S.alive[p] = 0;
 }
+#endif
 
 // field.py:103-112 orthonormal_frames + render.py:187-195 _cosine_dirs
 __device__ __forceinline__ d3 cosine_dir(d3 n, double u0, double u1) {
@@ -258,6 +268,7 @@ struct TraceGradOp : TraceStepOp {
 
 // normal + render.py:_hit_normals (127-141) + hit point, throughput, cosine
 // bounce (render.py:226-231) + slab test of the new ray
+#ifndef DDF_OPS_ONLY
 __global__ void bounce_kernel(const FieldDev* F, const WaveDev w, const PathState S, const int* list,
                               const int* count, int b) {
   const int n = *count;
@@ -303,8 +314,10 @@ __global__ void bounce_kernel(const FieldDev* F, const WaveDev w, const PathStat
     }
   }
 }
+#endif
 
 // render.py:233-242 over the bounce's alive list
+#ifndef DDF_OPS_ONLY
 __global__ void after_bounce_kernel(const WaveDev w, const PathState S, const int* list, const int* count) {
   const int n = *count;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -315,8 +328,10 @@ __global__ void after_bounce_kernel(const WaveDev w, const PathState S, const in
     }
   }
 }
+#endif
 
 // render.py:243  accum += radiance, in sample order
+#ifndef DDF_OPS_ONLY
 __global__ void film_kernel(const WaveDev w, const PathState S, double* accum) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= w.n_own) return;
@@ -325,5 +340,6 @@ __global__ void film_kernel(const WaveDev w, const PathState S, double* accum) {
   for (int s = 0; s < w.ns; ++s) a = dadd(a, S.rad[(int64_t)s * w.n_own + q]);
   accum[i] = a;
 }
+#endif
 
 }  // namespace ddf
