@@ -241,6 +241,10 @@ int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, 
 /* Diagnostics: tcgen05 engine pipeline wait-cycle counters, collected when
    the environment variable DDF_DEBUG_UMMA has bit 1 set (16 u64 values). */
 int ddf_debug_counters(uint64_t* out16, int32_t reset);
+/* Diagnostics: the tcgen05 engines' event timeline of CTA 0 (builds with
+   -DDDF_TRACE=1, empty otherwise): up to cap entries (clock64 << 16 | tag)
+   copied to out (host); returns the count. */
+int ddf_debug_trace(uint64_t* out, int32_t cap, int32_t reset);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ HEADER = os.path.join(ROOT, "include", "ddf_b200.h")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
-OBJ_DIR = os.path.join(HERE, "build")
+OBJ_DIR = os.path.join(HERE, "build")   # objects of the default flags; DDF_NVCC_EXTRA builds go to build/<tag>
 
 DDF_OK, DDF_EUSAGE, DDF_EDATA, DDF_ENUMERIC, DDF_ECUDA = 0, 1, 2, 3, 4
 PREC_FP32, PREC_BF16, PREC_FP32_SIMT = 0, 1, 2
@@ -34,7 +34,7 @@ STAGE_STEPS, STAGE_BOUNCES = 64, 32     # DDF_STAGE_STEPS, DDF_STAGE_BOUNCES
 EXPORTS = ("ddf_field_create", "ddf_field_add_network", "ddf_field_destroy", "ddf_field_set_precision",
            "ddf_last_error", "ddf_mlp_forward", "ddf_mlp_input_grad", "ddf_query", "ddf_trace",
            "ddf_normal", "ddf_render_path", "ddf_render_mode", "ddf_mesh_create", "ddf_mesh_intersect", "ddf_mesh_closest", "ddf_udf", "ddf_udf_grid", "ddf_rng_doubles", "ddf_compact",
-           "ddf_debug_counters")
+           "ddf_debug_counters", "ddf_debug_trace")
 
 
 def build(verbose: bool = False, force: bool = False) -> str:
@@ -49,10 +49,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(LIB_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     extra = os.environ.get("DDF_NVCC_EXTRA", "").split()
+    obj_dir = OBJ_DIR if not extra else os.path.join(OBJ_DIR, "_".join(x.strip("-").replace("=", "") for x in extra))
+    os.makedirs(obj_dir, exist_ok=True)
     objs, jobs = [], []
     for u in units:
         src = os.path.join(CSRC, u)
-        obj = os.path.join(OBJ_DIR, u[:-3] + ".o")
+        obj = os.path.join(obj_dir, u[:-3] + ".o")
         objs.append(obj)
         stale = force or not os.path.exists(obj) or os.path.getmtime(obj) < max(newest_header, os.path.getmtime(src))
         if stale:
@@ -164,6 +166,7 @@ def lib():
     L.ddf_mesh_intersect.argtypes = [vp, dp, dp, i64, ctypes.c_double, ctypes.c_double, dp, dp, dp, dp, vp]
     L.ddf_udf_grid.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32, i32, i32, dp, vp]
     L.ddf_debug_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), i32]
+    L.ddf_debug_trace.argtypes = [ctypes.POINTER(ctypes.c_uint64), i32, i32]
     for name in EXPORTS:
         if name != "ddf_last_error":
             getattr(L, name).restype = ctypes.c_int

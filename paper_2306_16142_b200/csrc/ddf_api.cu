@@ -1282,6 +1282,11 @@ int ddf_rng_doubles(const uint64_t state[2], const uint64_t inc[2], const uint64
   return DDF_OK;
 }
 
+int ddf_debug_trace(uint64_t* out, int32_t cap, int32_t reset) {
+  if (!out || cap < 0) return -1;
+  return engines::umma_debug_trace(reinterpret_cast<unsigned long long*>(out), cap, reset != 0);
+}
+
 int ddf_debug_counters(uint64_t* out16, int32_t reset) {
   unsigned long long h[16];
   engines::umma_debug_counters(h, reset != 0);

@@ -4,6 +4,7 @@
 #pragma once
 #define DDF_OPS_ONLY 1
 #include "engines.h"
+#include "mlp_2sm.cuh"
 #include "mlp_x3.cuh"
 
 namespace ddf {
@@ -12,6 +13,10 @@ namespace engines {
 template <class Op>
 int umma_launch(const FieldDev& F, const std::vector<umma::NetImage>& images, const Op& op, int max_rows,
                 int sm_count, uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
+  // one network wider than 256: the CTA-pair engine (mlp_2sm.cuh); DDF_DEBUG_UMMA
+  // bit 4096 keeps the single-CTA engine (A/B timing)
+  if (F.n_obj == 1 && images.size() == 1 && !images[0].host.pp && !(umma::debug_bits() & 4096) && sm_count >= 2)
+    return umma::launch_2sm<Op>(F, images[0], op, max_rows, sm_count, mask_scratch, st, err);
   return umma::launch<Op>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
 }
 
@@ -65,7 +70,8 @@ int simt_launch(const FieldDev& F, const Op& op, int max_rows, int max_width, in
   template int ddf::engines::simt_launch<OP>(const ddf::FieldDev&, const OP&, int, int, int, cudaStream_t,   \
                                              std::string*);
 
-// the diagnostics counters of this TU's module, under a TU-specific name
+// the diagnostics counters and event trace of this TU's module, under
+// TU-specific names
 #define DDF_UMMA_DEBUG_READER(NAME)                                                                         \
   namespace ddf { namespace engines {                                                                       \
   void NAME(unsigned long long* acc, bool reset) {                                                          \
@@ -76,4 +82,17 @@ int simt_launch(const FieldDev& F, const Op& op, int max_rows, int max_width, in
       for (int i = 0; i < 16; ++i) h[i] = 0;                                                                \
       cudaMemcpyToSymbol(umma::g_dbg, h, sizeof(h));                                                        \
     }                                                                                                       \
+  }                                                                                                         \
+  int NAME##_trace(unsigned long long* out, int cap, bool reset) {                                          \
+    std::vector<unsigned long long> all(umma::TRACE_CAP);                                                   \
+    if (cudaMemcpyFromSymbol(all.data(), umma::g_trace, sizeof(unsigned long long) * umma::TRACE_CAP) !=    \
+        cudaSuccess) return 0;                                                                              \
+    int n = 0;                                                                                              \
+    for (unsigned long long v : all)                                                                        \
+      if (v && n < cap) out[n++] = v;                                                                       \
+    if (reset) {                                                                                            \
+      std::vector<unsigned long long> z(umma::TRACE_CAP, 0ull);                                             \
+      cudaMemcpyToSymbol(umma::g_trace, z.data(), sizeof(unsigned long long) * umma::TRACE_CAP);            \
+    }                                                                                                       \
+    return n;                                                                                               \
   } } }

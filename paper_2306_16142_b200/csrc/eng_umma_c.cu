@@ -8,6 +8,14 @@ namespace ddf {
 namespace engines {
 void umma_debug_a(unsigned long long*, bool);
 void umma_debug_b(unsigned long long*, bool);
+int umma_debug_a_trace(unsigned long long*, int, bool);
+int umma_debug_b_trace(unsigned long long*, int, bool);
+int umma_debug_trace(unsigned long long* out, int cap, bool reset) {
+  int n = umma_debug_a_trace(out, cap, reset);
+  n += umma_debug_b_trace(out + n, cap - n, reset);
+  n += umma_debug_c_trace(out + n, cap - n, reset);
+  return n;
+}
 void umma_debug_counters(unsigned long long* out16, bool reset) {
   for (int i = 0; i < 16; ++i) out16[i] = 0;
   umma_debug_a(out16, reset);

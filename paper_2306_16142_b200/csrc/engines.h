@@ -34,6 +34,8 @@ int simt_launch(const FieldDev& F, const Op& op, int max_rows, int max_width, in
 // diagnostics counters of the tcgen05 engines (DDF_PIPE_STATS builds), summed
 // over the engine translation units
 void umma_debug_counters(unsigned long long* out16, bool reset);
+// the event timeline of CTA 0 (DDF_TRACE builds): entries written, <= cap
+int umma_debug_trace(unsigned long long* out, int cap, bool reset);
 
 }  // namespace engines
 }  // namespace ddf

@@ -28,7 +28,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include "ddf_common.cuh"
 #include "field_kernels.cuh"
@@ -44,12 +46,36 @@ constexpr int ROWS = 128;
 constexpr bool kStats = DDF_PIPE_STATS != 0;
 // DDF_DEBUG_UMMA bits that skip work (timing experiments, wrong results):
 // honoured only in the diagnostics build (-DDDF_PIPE_STATS=1, scratch/).
-constexpr int kUnsafeDbg = 1 | 8 | 128 | 1024;
+// -DDDF_ALLOW_DBG=1 honours them without the counters (timeline builds).
+#ifndef DDF_ALLOW_DBG
+#define DDF_ALLOW_DBG 0
+#endif
+constexpr int kUnsafeDbg = 1 | 8 | 128 | 1024 | 2048;
 inline int debug_bits() {
   static const int raw = getenv("DDF_DEBUG_UMMA") ? atoi(getenv("DDF_DEBUG_UMMA")) : 0;
-  return kStats ? raw : (raw & ~kUnsafeDbg);
+  return (kStats || DDF_ALLOW_DBG) ? raw : (raw & ~kUnsafeDbg);
 }
 static __device__ unsigned long long g_dbg[16];   // per translation unit (engines.h sums them)
+// Event timeline of CTA 0 (diagnostics build -DDDF_TRACE=1): entries
+// (clock64 << 16) | tag, tag = event | step << 5 | half << 11 | role << 12,
+// recorded for the tiles CTA 0 runs as its TRACE_TILE0-th and next ones.
+#ifndef DDF_TRACE
+#define DDF_TRACE 0
+#endif
+constexpr bool kTrace = DDF_TRACE != 0;
+// Each recording thread owns a TRACE_PER_ROLE slice (plain stores, no
+// atomics, so the timeline is not perturbed by round trips); the reader
+// compacts the slices.
+constexpr int TRACE_CAP = 16384, TRACE_PER_ROLE = 4096, TRACE_TILE0 = 3, TRACE_TILES = 2;
+static __device__ unsigned long long g_trace[TRACE_CAP];
+struct TraceCursor {
+  int role, n;
+  __device__ void ev(bool on, int e, int step, int half) {
+    if (kTrace && on && n < TRACE_PER_ROLE)
+      g_trace[role * TRACE_PER_ROLE + n++] =
+          ((unsigned long long)clock64() << 16) | (unsigned)(e | (step << 5) | (half << 11) | (role << 12));
+  }
+};
 #define DDF_DBG_T0() long long _t0 = kStats ? clock64() : 0
 #define DDF_DBG_ADD(i) do { if (kStats) dbg_acc[i] += (unsigned long long)(clock64() - _t0); } while (0)
 #define DDF_DBG_FLUSH() do { if (kStats) for (int _i = 0; _i < 16; ++_i) if (dbg_acc[_i]) atomicAdd(&g_dbg[_i], dbg_acc[_i]); } while (0)
@@ -201,6 +227,50 @@ __device__ __forceinline__ void mma_k64_commit(uint32_t tmem_d, uint64_t da, uin
       "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t"
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(id), "r"(acc), "r"(bar)
+      : "memory");
+}
+
+// Warp-wide variants: all 32 lanes of the issuing warp execute them in
+// converged code (so the compiler keeps descriptors in uniform registers
+// without an ELECT / R2UR.BROADCAST waterfall) and one lane, chosen by
+// elect.sync inside the asm, issues.
+// Descriptors travel as their low 32 bits (start address >> 4, LBO): the
+// high word (SBO = 1024 B, version, 128-byte swizzle) is the same for every
+// operand here, so the K-step advances are 32-bit adds.
+constexpr uint32_t SDESC_HI = (uint32_t)((1024 >> 4) | (1u << 14) | (2u << 29));
+__device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr) { return ((saddr & 0x3FFFFu) >> 4) | (1u << 16); }
+__device__ __forceinline__ void mma_k64_commit_w(uint32_t tmem_d, uint32_t da, uint32_t db, uint32_t id,
+                                                 uint32_t acc, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, e;\n\t.reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
+      ".reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, %3, %3;\n\t"
+      "add.u32 x1, %1, 2;\n\tadd.u32 x2, %1, 4;\n\tadd.u32 x3, %1, 6;\n\t"
+      "add.u32 y1, %2, 2;\n\tadd.u32 y2, %2, 4;\n\tadd.u32 y3, %2, 6;\n\t"
+      "mov.b64 a0, {%1, %6};\n\tmov.b64 a1, {x1, %6};\n\tmov.b64 a2, {x2, %6};\n\tmov.b64 a3, {x3, %6};\n\t"
+      "mov.b64 b0, {%2, %6};\n\tmov.b64 b1, {y1, %6};\n\tmov.b64 b2, {y2, %6};\n\tmov.b64 b3, {y3, %6};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(tmem_d),
+      "r"(da), "r"(db), "r"(id), "r"(acc), "r"(bar), "n"(SDESC_HI)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit_w(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
 
@@ -627,16 +697,27 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
     }
   } else if (warp == 1) {
     // ================================================= MMA issuer
-    if (lane == 0) {
+    // The whole warp runs this loop in converged, warp-uniform control flow;
+    // each tcgen05 instruction is issued by one elected lane.  The chunk loop
+    // carries only the weight wait, the four-MMA issue and the ring advance:
+    // the issuing thread's instruction latency, not the tensor pipe, had
+    // paced this engine (~750 cycles per 512-cycle chunk with per-chunk
+    // bookkeeping in a lane-0 branch).
+    {
       DDF_DBG_T0();
+      TraceCursor tcur{1, 0};
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ar[2] = {0u, 0u};
       const uint64_t da0 = sdesc(a_base), db0 = sdesc(st_base);
+      const uint32_t da0_lo = sdesc_lo(a_base), db0_lo = sdesc_lo(st_base);
       const uint32_t sstep = (uint32_t)sstride >> 4;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         int j0, j1, base, nv;
         tile_rows(F, op, t, j0, j1, base, nv);
+        const bool trc = kTrace && blockIdx.x == 0 && lane == 0 &&
+                         (t - (int)blockIdx.x) / (int)gridDim.x >= TRACE_TILE0 &&
+                         (t - (int)blockIdx.x) / (int)gridDim.x < TRACE_TILE0 + TRACE_TILES;
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
           const int ns = kProgG ? P->n_grad : P->n_fwd;
@@ -645,59 +726,80 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
             const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
             const uint32_t id = idesc(st.rows);
             const bool wa = writes_a(st.epi);
-            const int c0 = min(st.nchunk - 1, ((st.N >> 1) - 1) >> 6);   // last chunk touching A cols < N/2
+            // chunks [0, kc1) read A columns < K/2 (A_READY(0)), the rest also
+            // columns >= K/2 (A_READY(1)); in the last N-half, A_FREE(0) follows
+            // chunk c0 (the last reading A columns < N/2) and A_FREE(1) the last
+            const int kc1 = min(st.nchunk, (st.K >> 1) >> 6);
+            const int c0 = min(st.nchunk - 1, ((st.N >> 1) - 1) >> 6);
+            const int nfull = st.K >> 6;                 // chunks of four K = 16 MMAs
             bool waited0 = false, waited1 = false;
+            auto wait_a = [&](int which) {
+              DDF_DBG_T0();
+              tcur.ev(trc, which ? 3 : 1, s, 0);
+              mbar_wait(BAR_A_READY(which), ar[which] & 1u);
+              ++ar[which];
+              tcur.ev(trc, which ? 4 : 2, s, 0);
+              if (lane == 0) DDF_DBG_ADD(0);
+            };
             if (st.rows > prev_rows) {
               // half 0 of this step would overwrite TMEM columns of the previous
               // step's half 1: wait until both previous epilogue halves are done
-              mbar_wait(BAR_A_READY(0), ar[0] & 1u); ++ar[0]; waited0 = true;
-              mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; waited1 = true;
+              wait_a(0); wait_a(1);
+              waited0 = waited1 = true;
             }
             prev_rows = st.rows;
             for (int h = 0; h < st.nh; ++h) {
-              for (int kc = 0; kc < st.nchunk; ++kc) {
-                const bool need1 = (kc * 64 + 63) >= (st.K >> 1);
-                {
-                  DDF_DBG_T0();
-                  if (!waited0) { mbar_wait(BAR_A_READY(0), ar[0] & 1u); ++ar[0]; waited0 = true; }
-                  if (need1 && !waited1) { mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; waited1 = true; }
-                  DDF_DBG_ADD(0);
-                }
-                {
-                  DDF_DBG_T0();
+              const uint32_t td = tmem + (uint32_t)(h * st.rows);
+              const bool last_half = h == st.nh - 1;
+              // chunk segments: [kc_a, kc_b) issued back to back, the waits and
+              // A_FREE commits between segments
+              int kc = 0;
+              while (kc < st.nchunk) {
+                if (kc == 0 && !waited0) { wait_a(0); waited0 = true; }
+                if (kc >= kc1 && !waited1) { wait_a(1); waited1 = true; }
+                int kend = st.nchunk;
+                if (!waited1 && kc1 > kc) kend = min(kend, kc1);
+                if (wa && last_half && c0 >= kc) kend = min(kend, c0 + 1);
+                const int kfull = min(kend, nfull);
+                if (kc == 0) tcur.ev(trc, 6, s, h);
+                for (; kc < kfull; ++kc) {
                   mbar_wait(BAR_FULL(stage), phase);
-                  DDF_DBG_ADD(1);
+                  tc_after_sync();
+                  if (kStats && (dbg & 128)) {   // dbg 128: timing experiment only, no MMAs (wrong results)
+                    tc_commit_w(BAR_EMPTY(stage));
+                  } else {
+                    mma_k64_commit_w(td, da0_lo + (uint32_t)(kc * (ROWS * 128 / 16)), db0_lo + (uint32_t)stage * sstep,
+                                     id, kc ? 1u : 0u, BAR_EMPTY(stage));
+                  }
+                  tcur.ev(trc, 8, s, h);                  // 8: K chunk issued
+                  if (++stage == n_stages) { stage = 0; phase ^= 1u; }
                 }
-                tc_after_sync();
-                const long long t_is = kStats ? clock64() : 0;
-                const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
-                const uint64_t da = da0 + (uint64_t)(kc * (ROWS * 128 / 16));
-                const uint64_t db = db0 + (uint64_t)(stage * sstep);
-                const uint32_t td = tmem + (uint32_t)(h * st.rows);
-                if (kStats && (dbg & 128)) {   // dbg 128: timing experiment only, no MMAs (wrong results)
-                  tc_commit(BAR_EMPTY(stage));
-                } else if (nks == 4) {
-                  mma_k64_commit(td, da, db, id, kc ? 1u : 0u, BAR_EMPTY(stage));
-                } else {
-                  for (int ks = 0; ks < nks; ++ks)
-                    mma_bf16(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
-                  tc_commit(BAR_EMPTY(stage));
+                if (kc < kend) {
+                  // the partial last chunk (K not a multiple of 64: the input layer)
+                  mbar_wait(BAR_FULL(stage), phase);
+                  tc_after_sync();
+                  const int nks = (st.K - kc * 64 + 15) >> 4;
+                  const uint64_t da = da0 + (uint64_t)(kc * (ROWS * 128 / 16));
+                  const uint64_t db = db0 + (uint64_t)(stage * sstep);
+                  for (int ks = 0; ks < nks; ++ks) mma_bf16_w(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
+                  tc_commit_w(BAR_EMPTY(stage));
+                  if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+                  ++kc;
                 }
-                if (wa && h == st.nh - 1) {
-                  if (kc == c0) tc_commit(BAR_A_FREE(0));
-                  if (kc == st.nchunk - 1) tc_commit(BAR_A_FREE(1));
+                if (wa && last_half) {
+                  if (kc == c0 + 1) tc_commit_w(BAR_A_FREE(0));
+                  if (kc == st.nchunk) tc_commit_w(BAR_A_FREE(1));
                 }
-                if (kStats) atomicAdd(&g_dbg[8], (unsigned long long)(clock64() - t_is));
-                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
               }
-              tc_commit(BAR_ACC(h));
+              tc_commit_w(BAR_ACC(h));
+              tcur.ev(trc, 7, s, h);                       // 7: last chunk of the half issued
             }
-            if (kStats) atomicAdd(&g_dbg[5], 1ull);
-            if (!waited1) { mbar_wait(BAR_A_READY(1), ar[1] & 1u); ++ar[1]; }   // keep phases in step
+            if (kStats && lane == 0) atomicAdd(&g_dbg[5], 1ull);
+            if (!waited1) wait_a(1);   // keep phases in step
           }
         }
       }
-      DDF_DBG_ADD(4);
+      if (lane == 0) DDF_DBG_ADD(4);
     }
   } else {
     // ================================================= row warps (encoding + epilogues)
@@ -708,6 +810,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
     const uint32_t a_row = a_base + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);   // this row in every A k-block
     uint32_t* my_masks = mask_scratch + (size_t)blockIdx.x * MASK_WORDS_PER_CTA;
     uint32_t acc_ph[2] = {0u, 0u}, free_ph[2] = {0u, 0u};
+    TraceCursor tcur{warp == EPI_WARP0 ? 2 : 3, 0};
     int staged_j = -1;   // network whose params are in shared memory
     // this row of the next tile: list entry and path state fetched one tile
     // ahead (issued once the current tile's encoding is stored, so the two
@@ -731,6 +834,10 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
       tile_rows(F, op, t, j0, j1, base, nv);
       const bool valid = r < nv;
       const int slot = valid ? n_slot : 0;
+      const bool trc = kTrace && blockIdx.x == 0 && lane == 0 && (warp == EPI_WARP0 || warp == EPI_WARP0 + 7) &&
+                       (t - (int)blockIdx.x) / (int)gridDim.x >= TRACE_TILE0 &&
+                       (t - (int)blockIdx.x) / (int)gridDim.x < TRACE_TILE0 + TRACE_TILES;
+      tcur.ev(trc, 16, 0, 0);                                  // 16: tile start (encoding begins)
       double pos[3] = {n_pos[0], n_pos[1], n_pos[2]}, az = n_az, pol = n_pol;
       double best = 0.0;
       int bobj = 0;
@@ -772,6 +879,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
         fence_async_smem();
         __syncwarp();
         if (lane == 0) { mbar_arrive(BAR_A_READY(0)); mbar_arrive(BAR_A_READY(1)); }
+        tcur.ev(trc, 20, 0, 0);                        // 20: encoding stored
         if (j == j0) fetch(t + gridDim.x);
 
         const int ns = kProgG ? P->n_grad : P->n_fwd;
@@ -793,11 +901,22 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
             }
             {
               DDF_DBG_T0();
+              tcur.ev(trc, 17, s, h);                  // 17: wait for the accumulator begins
               mbar_wait(BAR_ACC(h), acc_ph[h] & 1u);
+              tcur.ev(trc, 18, s, h);                  // 18: accumulator ready
               if (threadIdx.x == EPI_WARP0 * 32) DDF_DBG_ADD(2);
             }
             ++acc_ph[h];
             tc_after_sync();
+            if ((kStats || DDF_ALLOW_DBG) && (dbg & 2048)) {   // dbg 2048: timing only, no epilogue (wrong results)
+              tc_before_sync();
+              if (wa) {
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(BAR_A_READY(h));
+              }
+              continue;
+            }
             if (epi == E_BWD_OUT) {
               if (sub == 0) {
                 // d pred / d inputs for this row: st.rows (= k0) fp32 columns
@@ -855,6 +974,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
               __syncwarp();
               if (lane == 0) mbar_arrive(BAR_A_READY(h));
             }
+            tcur.ev(trc, 19, s, h);                    // 19: epilogue of the half done
           }
           if (epi == E_HEAD || (Op::kFused && epi == E_MASKG_A)) {
             S.red[sub * ROWS + r] = head_part;
@@ -1559,13 +1679,50 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// TMA descriptors of one network's weight image (forward + gradient
+// programs back to back), viewed as rows of 128 bytes: boxes of 128 rows
+// (16 KB, a stage) and of 8 rows (the N = 80 backward output step).
+struct Tmaps {
+  CUtensorMap box128, box8;
+};
+
 struct NetImage {
   void* dev = nullptr;       // Prog (device)
   void* img = nullptr;       // fwd + grad images
   void* params = nullptr;    // biases + head weights (fp32)
   int in_width = 0;
   Prog host{};
+  Tmaps tmaps{};             // over img (networks wider than 256: the CTA-pair engine, mlp_2sm.cuh)
 };
+
+// Tensor maps over a network's weight image (rows of 128 bytes), built once
+// per image on the host through the driver entry point (no libcuda link).
+inline int make_weight_tmaps(const void* img, size_t bytes, Tmaps* out, std::string* err) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      *err = "cuTensorMapEncodeTiled unavailable";
+      return 4;
+    }
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {16, (cuuint64_t)(bytes / 128)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int b = 0; b < 2; ++b) {
+    const cuuint32_t box[2] = {16, b == 0 ? 128u : 8u};
+    CUresult r = enc(b == 0 ? &out->box128 : &out->box8, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(img),
+                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { *err = "cuTensorMapEncodeTiled failed"; return 4; }
+  }
+  return 0;
+}
+
+
 
 inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
 
@@ -1706,6 +1863,8 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   P.params_floats = (int)params.size();
   P.img_fwd = reinterpret_cast<const uint8_t*>(out->img);
   P.img_grad = reinterpret_cast<const uint8_t*>(out->img) + fwd_bytes;
+  if (!P.pp)
+    if (int rc = make_weight_tmaps(out->img, total, &out->tmaps, err)) return rc;
   if (cudaMalloc(&out->dev, sizeof(Prog)) != cudaSuccess) { *err = "cudaMalloc (program) failed"; return 4; }
   if (cudaMemcpy(out->dev, &P, sizeof(Prog), cudaMemcpyHostToDevice) != cudaSuccess) { *err = "upload failed"; return 4; }
   return 0;
