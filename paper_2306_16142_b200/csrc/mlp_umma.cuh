@@ -117,6 +117,23 @@ __device__ __forceinline__ Step load_step(const Step* p) {
   return s;
 }
 
+// Warp-uniform copy of a value every lane of a converged warp already agrees
+// on.  ptxas keeps the result of redux.sync in a uniform register and then
+// computes everything derived from it (descriptor advances, loop counters,
+// barrier addresses) on the uniform datapath, so a tcgen05.mma whose operands
+// all come from such values is issued as one uniform instruction: no ELECT /
+// R2UR.BROADCAST waterfall per operand (~45 SASS instructions per four-MMA
+// block otherwise, which paced the N = 128 engines).  Used by the MMA
+// issuer warps on values loaded from memory (step descriptors, the TMEM
+// base address), which the compiler must otherwise assume differ per lane.
+__device__ __forceinline__ uint32_t uni(uint32_t x) { return __reduce_or_sync(0xffffffffu, x); }
+__device__ __forceinline__ int uni(int x) { return (int)__reduce_or_sync(0xffffffffu, (uint32_t)x); }
+// the fields of a step the MMA issuer uses, warp-uniform
+__device__ __forceinline__ void uni_step(Step& st) {
+  st.K = uni(st.K); st.N = uni(st.N); st.nh = uni(st.nh); st.epi = uni(st.epi);
+  st.nchunk = uni(st.nchunk); st.rows = uni(st.rows);
+}
+
 struct Prog {
   int n_fwd, n_grad;
   int k0;              // padded input width (multiple of 16)
@@ -149,6 +166,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// The same wait for a converged warp, leaving on a warp vote: the loop's exit
+// is warp-uniform by construction, so the compiler keeps the code after it
+// on the uniform datapath (see uni below); a per-lane exit makes ptxas treat
+// everything downstream as potentially divergent.
+__device__ __forceinline__ void mbar_wait_u(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "vote.sync.all.pred q, p, 0xffffffff;\n\t"
+      "@!q bra WAIT_%=;\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
@@ -257,6 +288,24 @@ __device__ __forceinline__ void mma_k64_commit_w(uint32_t tmem_d, uint32_t da, u
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(tmem_d),
       "r"(da), "r"(db), "r"(id), "r"(acc), "r"(bar), "n"(SDESC_HI)
+      : "memory");
+}
+__device__ __forceinline__ void mma_k64_w(uint32_t tmem_d, uint32_t da, uint32_t db, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, e;\n\t.reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
+      ".reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, %3, %3;\n\t"
+      "add.u32 x1, %1, 2;\n\tadd.u32 x2, %1, 4;\n\tadd.u32 x3, %1, 6;\n\t"
+      "add.u32 y1, %2, 2;\n\tadd.u32 y2, %2, 4;\n\tadd.u32 y3, %2, 6;\n\t"
+      "mov.b64 a0, {%1, %5};\n\tmov.b64 a1, {x1, %5};\n\tmov.b64 a2, {x2, %5};\n\tmov.b64 a3, {x3, %5};\n\t"
+      "mov.b64 b0, {%2, %5};\n\tmov.b64 b1, {y1, %5};\n\tmov.b64 b2, {y2, %5};\n\tmov.b64 b3, {y3, %5};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t}" ::"r"(tmem_d),
+      "r"(da), "r"(db), "r"(id), "r"(acc), "n"(SDESC_HI)
       : "memory");
 }
 __device__ __forceinline__ void mma_bf16_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -1436,7 +1485,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
   float* sparams = reinterpret_cast<float*>(tmem_slot + 4);      // one copy: [params_bytes/4]
   (void)params_bytes;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t bar0 = smem_u32(bars);
   auto BAR_A_READY = [&](int sl) { return bar0 + 8u * sl; };
   auto BAR_ACC = [&](int sl) { return bar0 + 8u * (NSL + sl); };
@@ -1497,59 +1546,87 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
       }
     }
   } else if (warp == 1) {
-    // ================================================= MMA issuer: chunk-major over the four slots
-    if (lane == 0) {
+    // ================================================= MMA issuer: slot-major within a layer.
+    // Layer s of slot 0 (all its K chunks), then of slot 1, ...: slot 0's
+    // accumulator is committed after its own 8 MMAs, so its epilogue runs
+    // under the MMAs of slots 1-3 and its next layer can follow slot 3's
+    // directly.  (Chunk-major order committed all four accumulators at the
+    // end of the layer: MMA phase, then epilogue phase, nothing overlapped.)
+    // The layer's weight chunks stay in the ring until slot NSL-1 has read
+    // them (nchunk <= 2 stages; the ring has >= 4).  The whole warp runs this
+    // loop converged; one elected lane issues (see mma_k64_commit_w).
+    {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t ar[NSL];
-      for (int i = 0; i < NSL; ++i) ar[i] = 0u;
+      uint32_t ar = 0u;                              // A_READY phase: every slot completes one per step
       const long long t_all = kStats ? clock64() : 0;
-      for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
+      const uint32_t tmem_u = uni(tmem);
+      const uint32_t a0_lo = uni(sdesc_lo(a_base0)), db0_lo = uni(sdesc_lo(st_base));
+      const uint32_t a_step = uni((uint32_t)a_bytes >> 4), sstep = uni((uint32_t)stage_bytes >> 4);
+      const uint32_t bars_u = uni(bar0);
+      const int nst = uni(n_stages), packs_u = uni(packs);
+      TraceCursor tcur{1, 0};
+      for (int pk = blockIdx.x; pk < packs_u; pk += gridDim.x) {
         int j0, j1, base, nv;
         pp_rows<Op, NSL>(F, op, pk, 0, j0, j1, base, nv);
+        j0 = uni(j0);
+        j1 = uni(j1);
+        const bool trc = kTrace && blockIdx.x == 0 && lane == 0 && (pk - (int)blockIdx.x) / (int)gridDim.x >= TRACE_TILE0 &&
+                         (pk - (int)blockIdx.x) / (int)gridDim.x < TRACE_TILE0 + TRACE_TILES;
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
-          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+          const int ns = uni(__ldg(Op::kGrad ? &P->n_grad : &P->n_fwd));
           for (int s = 0; s < ns; ++s) {
-            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            uni_step(st);
             const uint32_t id = idesc(st.rows);
-            for (int kc = 0; kc < st.nchunk; ++kc) {
+            const int nfull = st.K >> 6;                 // chunks of four K = 16 MMAs
+#pragma unroll
+            for (int sl = 0; sl < NSL; ++sl) {
               {
+                // this slot's A tile is written and its TMEM columns are read out
                 DDF_DBG_T0();
-                mbar_wait(BAR_FULL(stage), phase);
-                DDF_DBG_ADD(1);
+                tcur.ev(trc, 1, s * NSL + sl, 0);            // 1: wait for the slot's A tile begins
+                mbar_wait_u(bars_u + 8u * sl, ar & 1u);
+                tcur.ev(trc, 2, s * NSL + sl, 0);            // 2: A tile ready
+                if (lane == 0) DDF_DBG_ADD(0);
               }
               tc_after_sync();
-              const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
-              const uint32_t b_chunk = st_base + (uint32_t)(stage * stage_bytes);
-#pragma unroll 1
-              for (int sl = 0; sl < NSL; ++sl) {
-                if (kc == 0) {
-                  // this slot's A tile is written and its TMEM columns are read out
+              const uint32_t da_lo = a0_lo + (uint32_t)sl * a_step;
+              const uint32_t td = tmem_u + (uint32_t)(sl * (512 / NSL));
+              int stg = stage;
+              uint32_t ph = phase;
+              for (int kc = 0; kc < st.nchunk; ++kc) {
+                if (sl == 0) {
                   DDF_DBG_T0();
-                  mbar_wait(BAR_A_READY(sl), ar[sl] & 1u);
-                  DDF_DBG_ADD(0);
-                  ++ar[sl];
+                  mbar_wait_u(bars_u + 8u * (uint32_t)(2 * NSL + stg), ph);
+                  if (lane == 0) DDF_DBG_ADD(1);
                   tc_after_sync();
                 }
-                const uint64_t da = sdesc(a_base0 + (uint32_t)(sl * a_bytes)) + (uint64_t)(kc * (ROWS * 128 / 16));
-                const uint64_t db = sdesc(b_chunk);
-                const uint32_t td = tmem + (uint32_t)(sl * (512 / NSL));
-                if (nks == 4) {
-                  if (kc == st.nchunk - 1) mma_k64_commit(td, da, db, id, kc ? 1u : 0u, BAR_ACC(sl));
-                  else mma_k64(td, da, db, id, kc ? 1u : 0u);
+                const uint32_t da = da_lo + (uint32_t)(kc * (ROWS * 128 / 16));
+                const uint32_t db = db0_lo + (uint32_t)stg * sstep;
+                if (kc < nfull) {
+                  mma_k64_w(td, da, db, id, kc ? 1u : 0u);
                 } else {
-                  for (int ks = 0; ks < nks; ++ks) mma_bf16(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
-                  if (kc == st.nchunk - 1) tc_commit(BAR_ACC(sl));
+                  const int nks = (st.K - kc * 64 + 15) >> 4;
+                  for (int ks = 0; ks < nks; ++ks)
+                    mma_bf16_w(td, ((uint64_t)SDESC_HI << 32) | (da + 2 * ks), ((uint64_t)SDESC_HI << 32) | (db + 2 * ks), id,
+                               (kc | ks) ? 1u : 0u);
                 }
+                if (++stg == nst) { stg = 0; ph ^= 1u; }
               }
-              tc_commit(BAR_EMPTY(stage));
-              if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              tc_commit_w(bars_u + 8u * (uint32_t)(NSL + sl));
+              tcur.ev(trc, 7, s * NSL + sl, 0);              // 7: the slot's layer issued
+            }
+            ++ar;
+            for (int kc = 0; kc < st.nchunk; ++kc) {     // every slot has read the layer's chunks
+              tc_commit_w(bars_u + 8u * (uint32_t)(2 * NSL + nst + stage));
+              if (++stage == nst) { stage = 0; phase ^= 1u; }
             }
           }
         }
       }
-      if (kStats) dbg_acc[4] += (unsigned long long)(clock64() - t_all);
+      if (kStats && lane == 0) dbg_acc[4] += (unsigned long long)(clock64() - t_all);
     }
   } else {
     // ================================================= row warps: group g (four warps, one per TMEM
@@ -1566,10 +1643,15 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
     int staged = -1;
     const bool w0 = kStats && threadIdx.x == EPI_WARP0 * 32;
     const long long t_rows = kStats ? clock64() : 0;
+    TraceCursor tcur{q == 0 && sl == 0 ? 2 : 3, 0};
     for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
       long long t_ph = kStats ? clock64() : 0;
       int j0, j1, base, nv;
       pp_rows<Op, NSL>(F, op, pk, sl, j0, j1, base, nv);
+      const bool trc = kTrace && blockIdx.x == 0 && lane == 0 && q == 0 && (sl == 0 || sl == NSL - 1) &&
+                       (pk - (int)blockIdx.x) / (int)gridDim.x >= TRACE_TILE0 &&
+                       (pk - (int)blockIdx.x) / (int)gridDim.x < TRACE_TILE0 + TRACE_TILES;
+      tcur.ev(trc, 16, sl, 0);                                   // 16: pack start (load path state)
       const bool valid = r < nv;
       int slot_id = 0;
       double pos[3] = {0.0, 0.0, 0.0}, az = 0.0, pol = 0.0, best = 0.0;
@@ -1612,6 +1694,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
         tc_before_sync();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR_A_READY(sl));
+        tcur.ev(trc, 20, sl, 0);                                 // 20: encoding stored
         if (w0) { dbg_acc[5] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
 
         const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
@@ -1619,7 +1702,9 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
         for (int s = 0; s < ns; ++s) {
           const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
           const int epi = st.epi;
+          tcur.ev(trc, 17, s * NSL + sl, 0);                     // 17: wait for the accumulator begins
           mbar_wait(BAR_ACC(sl), acc_ph & 1u);
+          tcur.ev(trc, 18, s * NSL + sl, 0);                     // 18: accumulator ready
           if (w0) { dbg_acc[2] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
           ++acc_ph;
           tc_after_sync();
@@ -1664,6 +1749,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
             if (F.composite) pv = dmul(net.scale, pv);
             if (j == j0 || pv < best) { best = pv; bobj = j; }
           }
+          tcur.ev(trc, 19, s * NSL + sl, 0);                     // 19: epilogue done
           if (w0) { dbg_acc[7] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
         }
       }
