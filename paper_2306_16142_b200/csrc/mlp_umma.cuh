@@ -1454,14 +1454,100 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
 // network changes.
 constexpr int QS = 4;                                    // most slots per CTA (mask scratch sizing)
 
+// Whole-row epilogue of the quad engine: the accumulator in 16-column pieces,
+// the next piece's TMEM load in flight while this one is processed.  The
+// per-piece chain (TMEM load -> bias, ReLU, pack -> shared stores) is
+// latency-bound (~700 cycles per 32 columns when run back to back, with
+// ~80 instructions issued), and 18 warps leave 96 registers per thread, so
+// the pipeline uses 2 x 16 accumulator registers instead of 1 x 32.
+template <int EPI, int NCH>
+__device__ __forceinline__ void epi_rows16(const Step& st, int r, uint32_t tmem_row, uint32_t a_row, uint32_t* my_masks,
+                                           const float* head_w, float& head_part, const float* sparams) {
+  const int r7 = r & 7;
+  const uint32_t bias_s = smem_u32(sparams) + 4u * (uint32_t)(size_t)st.bias;
+  const uint32_t head_s = smem_u32(head_w);
+  uint32_t rg[2][16];
+  uint32_t mw = 0u, mq = 0u;
+  DDF_TMEM_LD16(tmem_row, rg[0]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int c = i * 16;
+    if (i + 1 < NCH) DDF_TMEM_LD16(tmem_row + (uint32_t)(c + 16), rg[(i + 1) & 1]);
+    const uint32_t(&x)[16] = rg[i & 1];
+    float4 bq[4];
+    if constexpr (EPI != E_BWD_MASK_A) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) bq[k] = ld_shared_f4(bias_s + 4u * (uint32_t)(c + 4 * k));
+    } else if ((i & 1) == 0) {
+      mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
+    }
+    const float* bf = reinterpret_cast<const float*>(bq);
+    uint32_t pkd[8];
+    if constexpr (EPI == E_BWD_MASK_A) {
+      const uint32_t m = mq >> (16 * (i & 1));
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        pkd[e] = pack_bf16(((m >> (2 * e)) & 1u) ? __uint_as_float(x[2 * e]) : 0.f,
+                           ((m >> (2 * e + 1)) & 1u) ? __uint_as_float(x[2 * e + 1]) : 0.f);
+    } else if constexpr (EPI == E_RELU_A) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        pkd[e] = pack_bf16_relu(__uint_as_float(x[2 * e]) + bf[2 * e], __uint_as_float(x[2 * e + 1]) + bf[2 * e + 1]);
+    } else if constexpr (EPI == E_HEAD) {
+#pragma unroll
+      for (int e = 0; e < 16; e += 4) {
+        const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
+        head_part = fmaf(fmaxf(__uint_as_float(x[e]) + bf[e], 0.f), hw.x, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(x[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(x[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(x[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+      }
+    } else {
+      // ReLU mask bits (neural.py:241 "h > 0"), one u32 per 32 columns
+      uint32_t mh = 0u;
+      float v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float z = __uint_as_float(x[e]) + bf[e];
+        mh |= (z > 0.f ? 1u : 0u) << e;
+        v[e] = z;
+      }
+      mw |= mh << (16 * (i & 1));
+      if constexpr (EPI == E_RELU_MASK_A) {
+        if (i & 1) { my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw; mw = 0u; }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pkd[e] = pack_bf16_relu(v[2 * e], v[2 * e + 1]);
+      } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
+          v[e] = ((mh >> e) & 1u) ? hw.x : 0.f;
+          v[e + 1] = ((mh >> (e + 1)) & 1u) ? hw.y : 0.f;
+          v[e + 2] = ((mh >> (e + 2)) & 1u) ? hw.z : 0.f;
+          v[e + 3] = ((mh >> (e + 3)) & 1u) ? hw.w : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+      }
+    }
+    if constexpr (EPI != E_HEAD) {
+      const uint32_t blk = a_row + (uint32_t)((c >> 6) * (ROWS * 128));
+      const int cc0 = (c & 63) >> 3;
+      st_shared_v4(blk + (uint32_t)(((cc0) ^ r7) << 4), pkd[0], pkd[1], pkd[2], pkd[3]);
+      st_shared_v4(blk + (uint32_t)(((cc0 + 1) ^ r7) << 4), pkd[4], pkd[5], pkd[6], pkd[7]);
+    }
+    if (i + 1 < NCH) tmem_wait_ld();
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epi_rows_n(int nm, const Step& st, int r, uint32_t tmem_row, uint32_t a_row,
                                            uint32_t* my_masks, const float* head_w, float& head_part,
                                            const float* sp) {
-  switch (nm) {
-    case 2: epi_direct<EPI, 2, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
-    case 4: epi_direct<EPI, 4, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
-    case 8: epi_direct<EPI, 8, 32>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+  switch (nm) {   // nm: 32-column groups of the layer (64 / 128 wide)
+    case 2: epi_rows16<EPI, 4>(st, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
+    case 4: epi_rows16<EPI, 8>(st, r, tmem_row, a_row, my_masks, head_w, head_part, sp); break;
     default: break;
   }
 }
