@@ -66,6 +66,26 @@ __device__ __forceinline__ void dir_u34(d3 d, double& u3, double& u4) {
   encode_angles(az, pol, u3, u4);
 }
 
+// Encoded angle inputs of a query direction the way query_batch forms them:
+// vecs_to_angles (field.py:258), then _predict's re-canonicalisation
+// angles -> unit vector -> angles (field.py:251).  Away from the poles and
+// the azimuth wrap the second pass returns the first pass's angles to within
+// a few f64 ulps (it exists to canonicalise az at the poles and at 0 = 2 pi),
+// far below the fp32 / tf32-split / bf16 rounding every engine applies to the
+// inputs; there the first pass is used directly.  That halves the f64
+// trigonometry per ray (2 atan2 + 2 acos + 2 sincos -> 1 + 1), which bounded
+// the <= 128-wide query: ~9 K of 25 K cycles per 512-row pack.  Near a pole
+// (sin pol < 1e-3) or the wrap (az within 1e-6 of 0 or 2 pi) the reference's
+// exact sequence runs.
+__device__ __forceinline__ void query_dir_u34(d3 d, double& u3, double& u4) {
+  double a0, a1;
+  dir_angles(d, a0, a1);
+  const double two_pi = 6.283185307179586;
+  const bool edge = !(a1 > 1e-3 && a1 < 3.1405926535897933 && a0 > 1e-6 && a0 < two_pi - 1e-6);
+  if (edge) dir_u34(angles_dir(a0, a1), u3, u4);
+  else encode_angles(a0, a1, u3, u4);
+}
+
 __device__ __forceinline__ d3 ld3(const double* a, int64_t i) { return mk3(a[3 * i], a[3 * i + 1], a[3 * i + 2]); }
 __device__ __forceinline__ void st3(double* a, int64_t i, d3 v) { a[3 * i] = v.x; a[3 * i + 1] = v.y; a[3 * i + 2] = v.z; }
 
@@ -114,9 +134,7 @@ struct QueryOp : ListBase {
   __device__ void load(int s, double* p, double& u3, double& u4) const {
     const d3 q = ld3(pos, s);
     p[0] = q.x; p[1] = q.y; p[2] = q.z;
-    double a0, a1;
-    dir_angles(ld3(dirs, s), a0, a1);          // field.py:258
-    dir_u34(angles_dir(a0, a1), u3, u4);       // field.py:251 re-canonicalise
+    query_dir_u34(ld3(dirs, s), u3, u4);
   }
   __device__ void store_fwd(int s, double pred, int obj) const {
     const double c = fmin(fmax(pred, -delta), delta);   // field.py:253

@@ -1730,6 +1730,23 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
     const bool w0 = kStats && threadIdx.x == EPI_WARP0 * 32;
     const long long t_rows = kStats ? clock64() : 0;
     TraceCursor tcur{q == 0 && sl == 0 ? 2 : 3, 0};
+    // this row of the slot's next tile: list entry and path state (with its
+    // f64 direction -> angle trigonometry) fetched one pack ahead, issued
+    // once the current pack's encoding is stored, so the loads and the trig
+    // run while the row warp would otherwise wait for layer accumulators
+    int n_slot = 0;
+    double n_pos[3] = {0.0, 0.0, 0.0}, n_az = 0.0, n_pol = 0.0;
+    auto fetch = [&](int pp) {
+      if (pp < packs) {
+        int a0, a1, b0, c0;
+        pp_rows<Op, NSL>(F, op, pp, sl, a0, a1, b0, c0);
+        if (r < c0) {
+          n_slot = op.slot(b0 + r);
+          if constexpr (!Op::kRaw) op.load(n_slot, n_pos, n_az, n_pol);
+        }
+      }
+    };
+    fetch(blockIdx.x);
     for (int pk = blockIdx.x; pk < packs; pk += gridDim.x) {
       long long t_ph = kStats ? clock64() : 0;
       int j0, j1, base, nv;
@@ -1737,15 +1754,11 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
       const bool trc = kTrace && blockIdx.x == 0 && lane == 0 && q == 0 && (sl == 0 || sl == NSL - 1) &&
                        (pk - (int)blockIdx.x) / (int)gridDim.x >= TRACE_TILE0 &&
                        (pk - (int)blockIdx.x) / (int)gridDim.x < TRACE_TILE0 + TRACE_TILES;
-      tcur.ev(trc, 16, sl, 0);                                   // 16: pack start (load path state)
+      tcur.ev(trc, 16, sl, 0);                                   // 16: pack start
       const bool valid = r < nv;
-      int slot_id = 0;
-      double pos[3] = {0.0, 0.0, 0.0}, az = 0.0, pol = 0.0, best = 0.0;
+      const int slot_id = valid ? n_slot : 0;
+      double pos[3] = {n_pos[0], n_pos[1], n_pos[2]}, az = n_az, pol = n_pol, best = 0.0;
       int bobj = 0;
-      if (valid) {
-        slot_id = op.slot(base + r);
-        if constexpr (!Op::kRaw) op.load(slot_id, pos, az, pol);
-      }
       if (w0) { dbg_acc[3] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
       for (int j = j0; j < j1; ++j) {
         const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
@@ -1781,6 +1794,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR_A_READY(sl));
         tcur.ev(trc, 20, sl, 0);                                 // 20: encoding stored
+        if (j == j0) fetch(pk + (int)gridDim.x);
         if (w0) { dbg_acc[5] += (unsigned long long)(clock64() - t_ph); t_ph = clock64(); }
 
         const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
