@@ -53,10 +53,11 @@ __device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
 // arrive, are visible before the MMAs read them
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, q;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "vote.sync.all.pred q, p, 0xffffffff;\n\t"
+      "@!q bra WAIT_%=;\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
@@ -138,7 +139,7 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
   S.red = reinterpret_cast<float*>(S.tmem_slot + 4);
   S.params = S.red + 2 * ROWS;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t rank = cluster_ctarank();
   const int pair = (int)(blockIdx.x >> 1), npairs = (int)(gridDim.x >> 1);
   const uint32_t bar0 = smem_u32(S.bars);
@@ -210,24 +211,37 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
     }
   } else if (warp == 1) {
     // ================================================= MMA issuer (leader CTA, whole warp)
+    // The whole warp runs this loop converged on warp-uniform values (uni,
+    // mbar_wait_u: mlp_umma.cuh), so the tcgen05 instructions are issued from
+    // uniform registers without per-operand ELECT / R2UR waterfalls.
     if (rank == 0) {
       TraceCursor tcur{1, 0};
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ar[2] = {0u, 0u};
-      const uint32_t da0_lo = sdesc_lo(a_base), db0_lo = sdesc_lo(st_base);
-      const uint32_t sstep = (uint32_t)stage_bytes >> 4;
-      for (int tp = pair; tp < pairs_total; tp += npairs) {
+      const uint32_t tmem_u = uni(tmem), bars_u = uni(bar0);
+      const uint32_t da0_lo = uni(sdesc_lo(a_base)), db0_lo = uni(sdesc_lo(st_base));
+      const uint32_t sstep = uni((uint32_t)stage_bytes >> 4);
+      const int nst = uni(n_stages), pairs_u = uni(pairs_total);
+      auto UB_A_READY = [&](int h) { return bars_u + 8u * (0 + h); };
+      auto UB_ACC = [&](int h) { return bars_u + 8u * (2 + h); };
+      auto UB_A_FREE = [&](int h) { return bars_u + 8u * (4 + h); };
+      auto UB_FULL = [&](int st_) { return bars_u + 8u * (uint32_t)(6 + st_); };
+      auto UB_EMPTY = [&](int st_) { return bars_u + 8u * (uint32_t)(6 + nst + st_); };
+      for (int tp = pair; tp < pairs_u; tp += npairs) {
         int j0, j1, base, nv;
         tile_rows2(F, op, 2 * tp, tiles, j0, j1, base, nv);
+        j0 = uni(j0);
+        j1 = uni(j1);
         const bool trc = kTrace && pair == 0 && lane == 0 && (tp - pair) / npairs >= TRACE_TILE0 &&
                          (tp - pair) / npairs < TRACE_TILE0 + TRACE_TILES;
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
-          const int ns = kProgG ? P->n_grad : P->n_fwd;
+          const int ns = uni(kProgG ? P->n_grad : P->n_fwd);
           int prev_rows = 1 << 30;
           for (int s = 0; s < ns; ++s) {
-            const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
+            Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
+            uni_step(st);
             const uint32_t id = idesc2(st.rows);
             const bool wa = writes_a(st.epi);
             const int kc1 = min(st.nchunk, (st.K >> 1) >> 6);
@@ -236,14 +250,14 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
             bool waited0 = false, waited1 = false;
             auto wait_a = [&](int which) {
               tcur.ev(trc, which ? 3 : 1, s, 0);
-              mbar_wait_cluster(BAR_A_READY(which), ar[which] & 1u);
+              mbar_wait_cluster(UB_A_READY(which), ar[which] & 1u);
               ++ar[which];
               tcur.ev(trc, which ? 4 : 2, s, 0);
             };
             if (st.rows > prev_rows) { wait_a(0); wait_a(1); waited0 = waited1 = true; }
             prev_rows = st.rows;
             for (int h = 0; h < st.nh; ++h) {
-              const uint32_t td = tmem + (uint32_t)(h * st.rows);
+              const uint32_t td = tmem_u + (uint32_t)(h * st.rows);
               const bool last_half = h == st.nh - 1;
               int kc = 0;
               while (kc < st.nchunk) {
@@ -255,30 +269,30 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
                 const int kfull = min(kend, nfull);
                 if (kc == 0) tcur.ev(trc, 6, s, h);
                 for (; kc < kfull; ++kc) {
-                  mbar_wait(BAR_FULL(stage), phase);
+                  mbar_wait_u(UB_FULL(stage), phase);
                   tc_after_sync();
                   mma2_k64_commit_w(td, da0_lo + (uint32_t)(kc * (ROWS * 128 / 16)), db0_lo + (uint32_t)stage * sstep,
-                                    id, kc ? 1u : 0u, BAR_EMPTY(stage));
+                                    id, kc ? 1u : 0u, UB_EMPTY(stage));
                   tcur.ev(trc, 8, s, h);
-                  if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+                  if (++stage == nst) { stage = 0; phase ^= 1u; }
                 }
                 if (kc < kend) {   // the partial last chunk (the input layer's K = 80)
-                  mbar_wait(BAR_FULL(stage), phase);
+                  mbar_wait_u(UB_FULL(stage), phase);
                   tc_after_sync();
                   const int nks = (st.K - kc * 64 + 15) >> 4;
                   const uint32_t da = da0_lo + (uint32_t)(kc * (ROWS * 128 / 16));
                   const uint32_t db = db0_lo + (uint32_t)stage * sstep;
                   for (int ks = 0; ks < nks; ++ks) mma2_bf16_w(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
-                  tc_commit2_w(BAR_EMPTY(stage));
-                  if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+                  tc_commit2_w(UB_EMPTY(stage));
+                  if (++stage == nst) { stage = 0; phase ^= 1u; }
                   ++kc;
                 }
                 if (wa && last_half) {
-                  if (kc == c0 + 1) tc_commit2_w(BAR_A_FREE(0));
-                  if (kc == st.nchunk) tc_commit2_w(BAR_A_FREE(1));
+                  if (kc == c0 + 1) tc_commit2_w(UB_A_FREE(0));
+                  if (kc == st.nchunk) tc_commit2_w(UB_A_FREE(1));
                 }
               }
-              tc_commit2_w(BAR_ACC(h));
+              tc_commit2_w(UB_ACC(h));
               tcur.ev(trc, 7, s, h);
             }
             if (!waited1) wait_a(1);   // keep phases in step

@@ -1063,25 +1063,35 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
 // ReLU-mask scratch and staged params.  The MMAs of a slot's step complete
 // before its epilogue writes the slot's A tile, so no a_free barriers exist.
 
+// One warp's NM 32-column chunks (STRIDE columns apart) of a slot's accumulator.
+// TMEM loads run one chunk ahead of the arithmetic (the chain TMEM load ->
+// bias/ReLU/pack -> shared stores is latency-bound when run back to back),
+// biases and head weights come through explicit ld.shared.
 template <int EPI, int NM, int STRIDE = 64>
 __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
                                            uint32_t* my_masks, const float* head_w, float& head_part,
                                            const float* sparams) {
   const int r7 = r & 7;
+  const uint32_t bias_s = smem_u32(sparams) + 4u * (uint32_t)(size_t)st.bias;
+  const uint32_t head_s = smem_u32(head_w);
+  uint32_t rgb[2][32];
+  DDF_TMEM_LD32(tmem_row + (uint32_t)c_first, rgb[0]);
+  uint32_t mq_next = 0u;
+  if constexpr (EPI == E_BWD_MASK_A) mq_next = my_masks[(st.mask_layer * 16 + (c_first >> 5)) * ROWS + r];
+  tmem_wait_ld();
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const int c = c_first + i * STRIDE;
-    uint32_t rg[32];
-    DDF_TMEM_LD32(tmem_row + (uint32_t)c, rg);
+    if (i + 1 < NM) DDF_TMEM_LD32(tmem_row + (uint32_t)(c + STRIDE), rgb[(i + 1) & 1]);
+    const uint32_t(&rg)[32] = rgb[i & 1];
     float4 bq[8];
-    uint32_t mq = 0u;
+    const uint32_t mq = mq_next;
     if constexpr (EPI != E_BWD_MASK_A) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) bq[k] = *reinterpret_cast<const float4*>(sparams + (size_t)st.bias + c + 4 * k);
+      for (int k = 0; k < 8; ++k) bq[k] = ld_shared_f4(bias_s + 4u * (uint32_t)(c + 4 * k));
     } else {
-      mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
+      if (i + 1 < NM) mq_next = my_masks[(st.mask_layer * 16 + ((c + STRIDE) >> 5)) * ROWS + r];
     }
-    tmem_wait_ld();
     const float* bf = reinterpret_cast<const float*>(bq);
     uint32_t pkd[16];
     if constexpr (EPI == E_BWD_MASK_A) {
@@ -1096,7 +1106,7 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
     } else if constexpr (EPI == E_HEAD) {
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
-        const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+        const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
         head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
         head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
         head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
@@ -1109,22 +1119,24 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
       for (int e = 0; e < 32; ++e) {
         const float z = __uint_as_float(rg[e]) + bf[e];
         mw |= (z > 0.f ? 1u : 0u) << e;
-        v[e] = fmaxf(z, 0.f);
+        v[e] = z;
       }
       if constexpr (EPI == E_RELU_MASK_A) {
         my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16_relu(v[2 * e], v[2 * e + 1]);
       } else {
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
-          const float4 hw = *reinterpret_cast<const float4*>(head_w + c + e);
+          const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
           v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
           v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
           v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
           v[e + 3] = ((mw >> (e + 3)) & 1u) ? hw.w : 0.f;
         }
-      }
 #pragma unroll
-      for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+        for (int e = 0; e < 16; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
+      }
     }
     if constexpr (EPI != E_HEAD) {
       const uint32_t blk = a_row + (uint32_t)((c >> 6) * (ROWS * 128));
@@ -1134,6 +1146,7 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
         st_shared_v4(blk + (uint32_t)(((cc0 + e) ^ r7) << 4), pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2],
                      pkd[4 * e + 3]);
     }
+    if (i + 1 < NM) tmem_wait_ld();
   }
 }
 
@@ -1199,7 +1212,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
   float* sparams = red + 4 * ROWS;                                // [2 slots][params_bytes/4]
   const int pfl = params_bytes >> 2;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t bar0 = smem_u32(bars);
   auto BAR_A_READY = [&](int sl) { return bar0 + 8u * sl; };
   auto BAR_ACC = [&](int sl) { return bar0 + 8u * (2 + sl); };
@@ -1258,43 +1271,56 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
       }
     }
   } else if (warp == 1) {
-    // ================================================= MMA issuer
-    if (lane == 0) {
+    // ================================================= MMA issuer (whole warp, converged, on
+    // warp-uniform values: see uni / mbar_wait_u)
+    {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t ar[2] = {0u, 0u};
-      const uint64_t db0 = sdesc(st_base);
-      for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+      uint32_t ar = 0u;                              // A_READY phase: each slot completes one per step
+      const uint32_t tmem_u = uni(tmem), bars_u = uni(bar0);
+      const uint32_t a0_lo = uni(sdesc_lo(a_base0)), db0_lo = uni(sdesc_lo(st_base));
+      const uint32_t a_step = uni((uint32_t)a_bytes >> 4), sstep = uni((uint32_t)stage_bytes >> 4);
+      const int nst = uni(n_stages), pairs_u = uni(pairs);
+      for (int pr = blockIdx.x; pr < pairs_u; pr += gridDim.x) {
         int j0, j1, base, nv;
         pp_rows(F, op, pr, 0, j0, j1, base, nv);
+        j0 = uni(j0);
+        j1 = uni(j1);
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
-          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+          const int ns = uni(__ldg(Op::kGrad ? &P->n_grad : &P->n_fwd));
           for (int s = 0; s < ns; ++s) {
-            const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            uni_step(st);
             const uint32_t id = idesc(st.rows);
+            const int nfull = st.K >> 6;
+#pragma unroll
             for (int sl = 0; sl < 2; ++sl) {
               // this slot's A tile (and its TMEM columns) are ready
-              mbar_wait(BAR_A_READY(sl), ar[sl] & 1u);
-              ++ar[sl];
-              const uint32_t a_slot = a_base0 + (uint32_t)(sl * a_bytes);
+              mbar_wait_u(bars_u + 8u * sl, ar & 1u);
+              tc_after_sync();
+              const uint32_t da_lo = a0_lo + (uint32_t)sl * a_step;
+              const uint32_t td = tmem_u + (uint32_t)(sl * 256);
               for (int kc = 0; kc < st.nchunk; ++kc) {
-                mbar_wait(BAR_FULL(stage), phase);
+                mbar_wait_u(bars_u + 8u * (uint32_t)(4 + stage), phase);
                 tc_after_sync();
-                const int nks = min(4, (st.K - kc * 64 + 15) >> 4);
-                const uint64_t da = sdesc(a_slot) + (uint64_t)(kc * (ROWS * 128 / 16));
-                const uint64_t db = db0 + (uint64_t)(stage * (stage_bytes >> 4));
-                const uint32_t td = tmem + (uint32_t)(sl * 256);
-                if (nks == 4) {
-                  mma_k64_commit(td, da, db, id, kc ? 1u : 0u, BAR_EMPTY(stage));
+                const uint32_t da = da_lo + (uint32_t)(kc * (ROWS * 128 / 16));
+                const uint32_t db = db0_lo + (uint32_t)stage * sstep;
+                const uint32_t bar_empty = bars_u + 8u * (uint32_t)(4 + nst + stage);
+                if (kc < nfull) {
+                  mma_k64_commit_w(td, da, db, id, kc ? 1u : 0u, bar_empty);
                 } else {
-                  for (int ks = 0; ks < nks; ++ks) mma_bf16(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
-                  tc_commit(BAR_EMPTY(stage));
+                  const int nks = (st.K - kc * 64 + 15) >> 4;
+                  for (int ks = 0; ks < nks; ++ks)
+                    mma_bf16_w(td, ((uint64_t)SDESC_HI << 32) | (da + 2 * ks), ((uint64_t)SDESC_HI << 32) | (db + 2 * ks), id,
+                               (kc | ks) ? 1u : 0u);
+                  tc_commit_w(bar_empty);
                 }
-                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+                if (++stage == nst) { stage = 0; phase ^= 1u; }
               }
-              tc_commit(BAR_ACC(sl));
+              tc_commit_w(bars_u + 8u * (uint32_t)(2 + sl));
             }
+            ++ar;
           }
         }
       }
@@ -1306,6 +1332,25 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
     const int r = q * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     uint32_t acc_ph[2] = {0u, 0u};
+    // this row of the next pair of tiles: list entries and path state fetched
+    // one pair ahead (issued once the current encodings are stored), so the
+    // dependent global round trips overlap the first layer's MMAs
+    int n_slot[2] = {0, 0};
+    double n_pos[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}}, n_az[2] = {0.0, 0.0}, n_pol[2] = {0.0, 0.0};
+    auto fetch = [&](int pp) {
+      if (pp < pairs) {
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          int a0, a1, b0, c0;
+          pp_rows(F, op, pp, sl, a0, a1, b0, c0);
+          if (r < c0) {
+            n_slot[sl] = op.slot(b0 + r);
+            if constexpr (!Op::kRaw) op.load(n_slot[sl], n_pos[sl], n_az[sl], n_pol[sl]);
+          }
+        }
+      }
+    };
+    fetch(blockIdx.x);
     for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
       int j0 = 0, j1 = 0;
       int slot_id[2] = {0, 0};
@@ -1317,12 +1362,10 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
         int base, nv;
         pp_rows(F, op, pr, sl, j0, j1, base, nv);
         valid[sl] = r < nv;
-        pos[sl][0] = pos[sl][1] = pos[sl][2] = 0.0;
-        az[sl] = pol[sl] = 0.0;
-        if (valid[sl]) {
-          slot_id[sl] = op.slot(base + r);
-          if constexpr (!Op::kRaw) op.load(slot_id[sl], pos[sl], az[sl], pol[sl]);
-        }
+        slot_id[sl] = valid[sl] ? n_slot[sl] : 0;
+        pos[sl][0] = n_pos[sl][0]; pos[sl][1] = n_pos[sl][1]; pos[sl][2] = n_pos[sl][2];
+        az[sl] = n_az[sl];
+        pol[sl] = n_pol[sl];
       }
       for (int j = j0; j < j1; ++j) {
         const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
@@ -1362,6 +1405,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
           __syncwarp();
           if (lane == 0) mbar_arrive(BAR_A_READY(sl));
         }
+        if (j == j0) fetch(pr + (int)gridDim.x);
 
         const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
         float head_part[2] = {0.f, 0.f};
