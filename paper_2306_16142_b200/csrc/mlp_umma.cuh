@@ -1281,11 +1281,14 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
       const uint32_t a0_lo = uni(sdesc_lo(a_base0)), db0_lo = uni(sdesc_lo(st_base));
       const uint32_t a_step = uni((uint32_t)a_bytes >> 4), sstep = uni((uint32_t)stage_bytes >> 4);
       const int nst = uni(n_stages), pairs_u = uni(pairs);
+      TraceCursor tcur{1, 0};
       for (int pr = blockIdx.x; pr < pairs_u; pr += gridDim.x) {
         int j0, j1, base, nv;
         pp_rows(F, op, pr, 0, j0, j1, base, nv);
         j0 = uni(j0);
         j1 = uni(j1);
+        const bool trc = kTrace && blockIdx.x == 0 && lane == 0 && (pr - (int)blockIdx.x) / (int)gridDim.x >= TRACE_TILE0 &&
+                         (pr - (int)blockIdx.x) / (int)gridDim.x < TRACE_TILE0 + TRACE_TILES;
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
           const int ns = uni(__ldg(Op::kGrad ? &P->n_grad : &P->n_fwd));
@@ -1297,7 +1300,9 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
 #pragma unroll
             for (int sl = 0; sl < 2; ++sl) {
               // this slot's A tile (and its TMEM columns) are ready
+              tcur.ev(trc, 1, s * 2 + sl, 0);                // 1: wait for the slot's A tile begins
               mbar_wait_u(bars_u + 8u * sl, ar & 1u);
+              tcur.ev(trc, 2, s * 2 + sl, 0);                // 2: A tile ready
               tc_after_sync();
               const uint32_t da_lo = a0_lo + (uint32_t)sl * a_step;
               const uint32_t td = tmem_u + (uint32_t)(sl * 256);
@@ -1319,6 +1324,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
                 if (++stage == nst) { stage = 0; phase ^= 1u; }
               }
               tc_commit_w(bars_u + 8u * (uint32_t)(2 + sl));
+              tcur.ev(trc, 7, s * 2 + sl, 0);                // 7: the slot's layer issued
             }
             ++ar;
           }
@@ -1351,7 +1357,12 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
       }
     };
     fetch(blockIdx.x);
+    TraceCursor tcur{warp == EPI_WARP0 ? 2 : 3, 0};
     for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+      const bool trc = kTrace && blockIdx.x == 0 && lane == 0 && (warp == EPI_WARP0 || warp == EPI_WARP0 + 7) &&
+                       (pr - (int)blockIdx.x) / (int)gridDim.x >= TRACE_TILE0 &&
+                       (pr - (int)blockIdx.x) / (int)gridDim.x < TRACE_TILE0 + TRACE_TILES;
+      tcur.ev(trc, 16, 0, 0);                                    // 16: pair of tiles starts
       int j0 = 0, j1 = 0;
       int slot_id[2] = {0, 0};
       bool valid[2] = {false, false};
@@ -1404,6 +1415,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
           tc_before_sync();
           __syncwarp();
           if (lane == 0) mbar_arrive(BAR_A_READY(sl));
+          tcur.ev(trc, 20, sl, 0);                               // 20: the slot's encoding stored
         }
         if (j == j0) fetch(pr + (int)gridDim.x);
 
@@ -1414,7 +1426,9 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
           const int epi = st.epi;
 #pragma unroll
           for (int sl = 0; sl < 2; ++sl) {
+            tcur.ev(trc, 17, s * 2 + sl, 0);                     // 17: wait for the accumulator begins
             mbar_wait(BAR_ACC(sl), acc_ph[sl] & 1u);
+            tcur.ev(trc, 18, s * 2 + sl, 0);                     // 18: accumulator ready
             ++acc_ph[sl];
             tc_after_sync();
             const uint32_t tmem_row = tmem + lane_addr + (uint32_t)(sl * 256);
@@ -1470,6 +1484,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
               }
               named_sync(1, N_EPI_WARPS * 32);
             }
+            tcur.ev(trc, 19, s * 2 + sl, 0);                     // 19: epilogue done
           }
         }
       }

@@ -16,7 +16,7 @@ from paper_2306_16142_b200 import _lib  # noqa: E402
 from paper_2306_16142_b200.field import CudaNeuralField  # noqa: E402
 from paper_2306_16142_b200.neural import kaiming_uniform  # noqa: E402
 
-NSL = 4
+NSL = 4   # slots per CTA: 4 (quad engine, <= 128 wide) or 2 (ping-pong engine, <= 256 wide); set from the widths
 
 
 def read_trace(reset=True):
@@ -57,6 +57,8 @@ def show(title, ev):
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 21
     widths = eval(sys.argv[2]) if len(sys.argv) > 2 else (5, 128, 128, 128, 128, 1)
+    global NSL
+    NSL = 4 if max(widths[1:-1]) <= 128 else 2
     torch.cuda.set_device(0)
     f = CudaNeuralField(kaiming_uniform(widths, 2), 10 / 0.98, precision="bf16")
     x = torch.rand(n, widths[0], dtype=torch.float64, device="cuda") * 2 - 1
