@@ -100,6 +100,27 @@ __device__ __forceinline__ void mma_ss(uint32_t tmem_d, uint64_t a, uint64_t b, 
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
+// One K-step of the split product in a single asm block for the converged
+// issuer warp (see umma::uni): TS(A_hi, W_hi), TS(A_hi, W_lo), SS(A_lo, W_hi)
+// and the commit that frees the weight stage.  Descriptors travel as their low
+// words; the high words (SBO, version, swizzle mode) are constants.
+constexpr uint32_t SDESC32_HI = (uint32_t)((256 >> 4) | (1u << 14) | (6u << 29));
+__device__ __forceinline__ void mma_x3_step_w(uint32_t tmem_d, uint32_t tmem_a, uint32_t bhi_lo, uint32_t blo_lo,
+                                              uint32_t alo_lo, uint32_t id, uint32_t acc, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, e;\n\t.reg .b64 bh, bl, al;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 q, %5, %5;\n\t"
+      "mov.b64 bh, {%2, %8};\n\tmov.b64 bl, {%3, %8};\n\tmov.b64 al, {%4, %9};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bl, %5, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, q;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "r"(bhi_lo), "r"(blo_lo), "r"(alo_lo), "r"(id), "r"(acc), "r"(bar), "n"(SDESC32_HI),
+      "n"(umma::SDESC_HI)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -271,7 +292,7 @@ mlp_x3_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
   S.red = reinterpret_cast<float*>(S.tmem_slot + 4);
   S.params = S.red + 2 * ROWS;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = umma::uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t bar0 = smem_u32(S.bars);
   auto BAR_A_READY = [&](int g) { return bar0 + 8u * g; };
   const uint32_t BAR_ACC = bar0 + 8u * GROUPS;
@@ -326,50 +347,50 @@ mlp_x3_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
       }
     }
   } else if (warp == 1) {
-    // ================================================= MMA issuer
-    if (lane == 0) {
+    // ================================================= MMA issuer (whole warp, converged, on
+    // warp-uniform values: umma::uni / umma::mbar_wait_u)
+    {
+      using umma::uni;
+      using umma::mbar_wait_u;
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t ar[GROUPS];
-#pragma unroll
-      for (int g = 0; g < GROUPS; ++g) ar[g] = 0u;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      uint32_t ar = 0u;                 // A_READY phase: every group completes one per step
+      const uint32_t tmem_u = uni(tmem), bars_u = uni(bar0);
+      const uint32_t alo0_lo = uni(umma::sdesc_lo(alo_base)), w0_lo = uni(umma::sdesc_lo(st_base));
+      const uint32_t sstep = uni((uint32_t)stage_bytes >> 4);
+      const int nst = uni(n_stages), tiles_u = uni(tiles);
+      for (int t = blockIdx.x; t < tiles_u; t += gridDim.x) {
         int j0, j1, base, nv;
         umma::tile_rows(F, op, t, j0, j1, base, nv);
+        j0 = uni(j0);
+        j1 = uni(j1);
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_x3);
-          const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
+          const int ns = uni(Op::kGrad ? P->n_grad : P->n_fwd);
           for (int s = 0; s < ns; ++s) {
-            const Step st = umma::load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            Step st = umma::load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            umma::uni_step(st);
             const uint32_t id = idesc_tf32(st.N);
-            const uint32_t d_t = tmem + (uint32_t)((s & 1) * REGION);
-            const uint32_t a_t = tmem + (uint32_t)(((s + 1) & 1) * REGION);
+            const uint32_t d_t = tmem_u + (uint32_t)((s & 1) * REGION);
+            const uint32_t a_t = tmem_u + (uint32_t)(((s + 1) & 1) * REGION);
             const int ngr = (st.K + 31) >> 5;
+            const uint32_t lo_off = (uint32_t)(st.N * 32) >> 4;   // W_lo block behind W_hi in a stage
             for (int kk = 0; kk < st.nchunk; ++kk) {
               const int g = kk >> 2;
-              if ((kk & 3) == 0) {
-                // A group g of this step: written by the previous epilogue (or the encoding)
-#pragma unroll
-                for (int gg = 0; gg < GROUPS; ++gg)
-                  if (gg == g) { mbar_wait(BAR_A_READY(gg), ar[gg] & 1u); ++ar[gg]; }
-              }
-              mbar_wait(BAR_FULL(stage), phase);
+              // A group g of this step: written by the previous epilogue (or the encoding)
+              if ((kk & 3) == 0) mbar_wait_u(bars_u + 8u * (uint32_t)g, ar & 1u);
+              mbar_wait_u(bars_u + 8u * (uint32_t)(GROUPS + 2 + stage), phase);
               tc_after_sync();
-              const uint32_t wb = st_base + (uint32_t)(stage * stage_bytes);
-              const uint64_t bhi = sdesc32(wb), blo = sdesc32(wb + (uint32_t)(st.N * 32));
-              const uint64_t alo = sdesc(alo_base + (uint32_t)(g * ROWS * 128 + (kk & 3) * 32));
-              const uint32_t ahi = a_t + (uint32_t)(kk * 8);
-              mma_ts(d_t, ahi, bhi, id, kk ? 1u : 0u);
-              mma_ts(d_t, ahi, blo, id, 1u);
-              mma_ss(d_t, alo, bhi, id, 1u);
-              tc_commit(BAR_EMPTY(stage));
-              if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              const uint32_t bhi = w0_lo + (uint32_t)stage * sstep;
+              const uint32_t alo = alo0_lo + (uint32_t)((g * ROWS * 128 + (kk & 3) * 32) >> 4);
+              mma_x3_step_w(d_t, a_t + (uint32_t)(kk * 8), bhi, bhi + lo_off, alo, id, kk ? 1u : 0u,
+                            bars_u + 8u * (uint32_t)(GROUPS + 2 + nst + stage));
+              if (++stage == nst) { stage = 0; phase ^= 1u; }
             }
             // groups this step does not read: consume their release to keep phases in step
-#pragma unroll
-            for (int gg = 0; gg < GROUPS; ++gg)
-              if (gg >= ngr) { mbar_wait(BAR_A_READY(gg), ar[gg] & 1u); ++ar[gg]; }
-            tc_commit(BAR_ACC);
+            for (int gg = ngr; gg < GROUPS; ++gg) mbar_wait_u(bars_u + 8u * (uint32_t)gg, ar & 1u);
+            ++ar;
+            umma::tc_commit_w(bars_u + 8u * (uint32_t)GROUPS);
           }
         }
       }
@@ -384,16 +405,28 @@ mlp_x3_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
     const uint32_t alo_row = alo_base + (uint32_t)((r >> 3) * 1024 + r7 * 128);
     uint32_t* my_masks = mask_scratch + (size_t)blockIdx.x * MASK_WORDS_PER_CTA;
     uint32_t acc_ph = 0u;
+    // this row of the next tile: list entry and path state (with its f64
+    // direction -> angle trigonometry) fetched one tile ahead, issued once
+    // the current tile's encoding is released
+    int n_slot = 0;
+    double n_pos[3] = {0.0, 0.0, 0.0}, n_u3 = 0.0, n_u4 = 0.0;
+    auto fetch = [&](int tt) {
+      if (tt < tiles) {
+        int a0, a1, b0, c0;
+        umma::tile_rows(F, op, tt, a0, a1, b0, c0);
+        if (r < c0) {
+          n_slot = op.slot(b0 + r);
+          if constexpr (!Op::kRaw) op.load(n_slot, n_pos, n_u3, n_u4);
+        }
+      }
+    };
+    fetch(blockIdx.x);
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int j0, j1, base, nv;
       umma::tile_rows(F, op, t, j0, j1, base, nv);
       const bool valid = r < nv;
-      int slot = 0;
-      double pos[3] = {0.0, 0.0, 0.0}, u3 = 0.0, u4 = 0.0;
-      if (valid) {
-        slot = op.slot(base + r);
-        if constexpr (!Op::kRaw) op.load(slot, pos, u3, u4);
-      }
+      const int slot = valid ? n_slot : 0;
+      double pos[3] = {n_pos[0], n_pos[1], n_pos[2]}, u3 = n_u3, u4 = n_u4;
       double best = 0.0;
       int bobj = 0;
       for (int j = j0; j < j1; ++j) {
@@ -434,6 +467,7 @@ mlp_x3_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
 #pragma unroll
         for (int g = 0; g < GROUPS; ++g)
           if ((g & 1) == sub) release_group(BAR_A_READY(g), lane);
+        if (j == j0) fetch(t + (int)gridDim.x);
 
         const int ns = Op::kGrad ? P->n_grad : P->n_fwd;
         float head_part = 0.f;
