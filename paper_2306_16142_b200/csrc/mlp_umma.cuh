@@ -1513,26 +1513,41 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
 // network changes.
 constexpr int QS = 4;                                    // most slots per CTA (mask scratch sizing)
 
-// Whole-row epilogue of the quad engine: the accumulator in 16-column pieces,
-// the next piece's TMEM load in flight while this one is processed.  The
-// per-piece chain (TMEM load -> bias, ReLU, pack -> shared stores) is
-// latency-bound (~700 cycles per 32 columns when run back to back, with
-// ~80 instructions issued), and 18 warps leave 96 registers per thread, so
-// the pipeline uses 2 x 16 accumulator registers instead of 1 x 32.
-template <int EPI, int NCH>
-__device__ __forceinline__ void epi_rows16(const Step& st, int r, uint32_t tmem_row, uint32_t a_row, uint32_t* my_masks,
-                                           const float* head_w, float& head_part, const float* sparams) {
+// Epilogue in 16-column pieces with the next piece's TMEM load in flight while
+// this one is processed: one warp's NM 32-column chunks, STRIDE columns apart
+// from c_first.  The per-piece chain (TMEM load -> bias, ReLU, pack -> shared
+// stores) is latency-bound (~700 cycles per 32 columns when run back to back,
+// ~80 instructions issued), and kernels with 16 row warps have 96 registers
+// per thread, so the pipeline holds 2 x 16 accumulator registers instead of
+// 1 x 32.  WAIT_FREE: the A columns may be overwritten only once the MMAs that
+// read them have completed (bar_free, the > 256-wide engines' a_free); the
+// wait sits before the first store, after the first piece's arithmetic.
+struct NoMid {
+  __device__ __forceinline__ void operator()() const {}
+};
+// mid(): called once the first 32-column chunk is stored (NM == 2 only), for
+// engines that release the A columns of a part in two steps.
+template <int EPI, int NM, int STRIDE, bool WAIT_FREE, class Mid = NoMid>
+__device__ __forceinline__ void epi_cols16(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
+                                           uint32_t* my_masks, const float* head_w, float& head_part,
+                                           const float* sparams, uint32_t bar_free, uint32_t& free_ph,
+                                           Mid mid = Mid()) {
+  constexpr bool WA = EPI != E_HEAD;
+  constexpr bool HEAD_DOT = EPI == E_HEAD || EPI == E_MASKG_HEAD_A;
   const int r7 = r & 7;
   const uint32_t bias_s = smem_u32(sparams) + 4u * (uint32_t)(size_t)st.bias;
   const uint32_t head_s = smem_u32(head_w);
   uint32_t rg[2][16];
   uint32_t mw = 0u, mq = 0u;
-  DDF_TMEM_LD16(tmem_row, rg[0]);
-  tmem_wait_ld();
+  if constexpr (NM > 0) {
+    DDF_TMEM_LD16(tmem_row + (uint32_t)c_first, rg[0]);
+    tmem_wait_ld();
+  }
 #pragma unroll
-  for (int i = 0; i < NCH; ++i) {
-    const int c = i * 16;
-    if (i + 1 < NCH) DDF_TMEM_LD16(tmem_row + (uint32_t)(c + 16), rg[(i + 1) & 1]);
+  for (int i = 0; i < 2 * NM; ++i) {
+    const int c = c_first + (i >> 1) * STRIDE + (i & 1) * 16;
+    if (i + 1 < 2 * NM)
+      DDF_TMEM_LD16(tmem_row + (uint32_t)(c_first + ((i + 1) >> 1) * STRIDE + ((i + 1) & 1) * 16), rg[(i + 1) & 1]);
     const uint32_t(&x)[16] = rg[i & 1];
     float4 bq[4];
     if constexpr (EPI != E_BWD_MASK_A) {
@@ -1577,10 +1592,17 @@ __device__ __forceinline__ void epi_rows16(const Step& st, int r, uint32_t tmem_
         if (i & 1) { my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r] = mw; mw = 0u; }
 #pragma unroll
         for (int e = 0; e < 8; ++e) pkd[e] = pack_bf16_relu(v[2 * e], v[2 * e + 1]);
-      } else {   // E_MASKG_A: d/dh of the last hidden layer = w_head * mask
+      } else {   // E_MASKG_A / E_MASKG_HEAD_A: d/dh of the last hidden layer = w_head * mask
 #pragma unroll
         for (int e = 0; e < 16; e += 4) {
           const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
+          if constexpr (HEAD_DOT) {
+            // the identity head of the forward, in E_HEAD's order (same fp32 result)
+            head_part = fmaf(fmaxf(v[e], 0.f), hw.x, head_part);
+            head_part = fmaf(fmaxf(v[e + 1], 0.f), hw.y, head_part);
+            head_part = fmaf(fmaxf(v[e + 2], 0.f), hw.z, head_part);
+            head_part = fmaf(fmaxf(v[e + 3], 0.f), hw.w, head_part);
+          }
           v[e] = ((mh >> e) & 1u) ? hw.x : 0.f;
           v[e + 1] = ((mh >> (e + 1)) & 1u) ? hw.y : 0.f;
           v[e + 2] = ((mh >> (e + 2)) & 1u) ? hw.z : 0.f;
@@ -1590,14 +1612,32 @@ __device__ __forceinline__ void epi_rows16(const Step& st, int r, uint32_t tmem_
         for (int e = 0; e < 8; ++e) pkd[e] = pack_bf16(v[2 * e], v[2 * e + 1]);
       }
     }
-    if constexpr (EPI != E_HEAD) {
+    if constexpr (WA) {
+      if constexpr (WAIT_FREE) {
+        if (i == 0) {
+          mbar_wait(bar_free, free_ph & 1u);
+          ++free_ph;
+        }
+      }
       const uint32_t blk = a_row + (uint32_t)((c >> 6) * (ROWS * 128));
       const int cc0 = (c & 63) >> 3;
       st_shared_v4(blk + (uint32_t)(((cc0) ^ r7) << 4), pkd[0], pkd[1], pkd[2], pkd[3]);
       st_shared_v4(blk + (uint32_t)(((cc0 + 1) ^ r7) << 4), pkd[4], pkd[5], pkd[6], pkd[7]);
+      if constexpr (NM == 2) {
+        if (i == 1) mid();
+      }
     }
-    if (i + 1 < NCH) tmem_wait_ld();
+    if (i + 1 < 2 * NM) tmem_wait_ld();
   }
+  if constexpr (WA && WAIT_FREE && NM == 0) ++free_ph;   // no columns in this part: keep the phase count in step
+}
+
+// the quad engine's whole-row epilogue: NCH 16-column pieces from column 0
+template <int EPI, int NCH>
+__device__ __forceinline__ void epi_rows16(const Step& st, int r, uint32_t tmem_row, uint32_t a_row, uint32_t* my_masks,
+                                           const float* head_w, float& head_part, const float* sparams) {
+  uint32_t unused = 0u;
+  epi_cols16<EPI, NCH / 2, 32, false>(st, 0, r, tmem_row, a_row, my_masks, head_w, head_part, sparams, 0u, unused);
 }
 
 template <int EPI>
