@@ -274,7 +274,8 @@ def bench_queries(args, rank, world, local):
             sweep.append({"precision": prc, "rows": big, "ms": t, "queries_per_s": big / (t / 1e3),
                           "tflops": F * big / (t / 1e3) / 1e12})
     out["sweep"] = sweep
-    out["sweep_note"] = ("5->4x128->1: 128-wide layers cap UMMA at N = 128, about half the bf16 tensor peak "
+    out["sweep_note"] = ("5->4x128->1 on the four-slot (quad) engine: N = 128 MMAs are full rate, the bound is the "
+                         "per-slot hand-off between epilogue and MMAs and the per-ray f64 angle trigonometry "
                          "(DESIGN.md section 3); fp32 runs 3xTF32 on tcgen05 (ceiling bf16 / 6)")
     if rank == 0:
         print(json.dumps(out))
