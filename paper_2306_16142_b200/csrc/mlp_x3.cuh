@@ -547,6 +547,316 @@ mlp_x3_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ================================================================== two tiles in flight (<= 128 wide)
+// Networks whose hidden layers are at most 128 wide (config 1, the UDF scan)
+// leave half of TMEM and of the A_lo buffer unused in mlp_x3_kernel, and with
+// one tile per CTA the tensor pipe idles through every epilogue (measured:
+// ~23 K cycles per tile against 9.6 K of MMAs).  Here two 128-row tiles
+// ("slots" X, Y) run the layers in lock-step, as in the bf16 ping-pong
+// engine: the MMA warp issues layer s of X, then layer s of Y, while the row
+// warps run X's epilogue.  Slot sl owns TMEM columns [256 sl, 256 sl + 256):
+// D_s in its 128-column region s & 1, A_hi in the other; its own A_lo buffer,
+// barriers, ReLU-mask scratch and staged params.  A slot's A is released
+// once per step (all groups at once): by the time the issuer returns to the
+// slot its epilogue is done, so the group-by-group release of the one-tile
+// kernel buys nothing here.
+constexpr int PP_REGION = 128;
+constexpr int PP_GROUPS = PP_REGION / 32;
+
+template <class Op>
+__global__ void __launch_bounds__(NTHREADS, 1)
+mlp_x3pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, int n_stages, int alo_bytes,
+                int stage_bytes, int params_bytes) {
+  using umma::uni;
+  using umma::mbar_wait_u;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base_ptr = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* alo = base_ptr;                                        // [2 slots][alo_bytes]
+  uint8_t* stages = base_ptr + 2 * (size_t)alo_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)n_stages * stage_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * n_stages);
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);           // [2 slots][2 subs][128]
+  float* sparams = red + 4 * ROWS;                                // [2 slots][params_bytes/4]
+  const int pfl = params_bytes >> 2;
+
+  const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;
+  const uint32_t bar0 = smem_u32(bars);
+  auto BAR_A_READY = [&](int sl) { return bar0 + 8u * sl; };
+  auto BAR_ACC = [&](int sl) { return bar0 + 8u * (2 + sl); };
+  auto BAR_FULL = [&](int st_) { return bar0 + 8u * (4 + st_); };
+  auto BAR_EMPTY = [&](int st_) { return bar0 + 8u * (4 + n_stages + st_); };
+
+  if (threadIdx.x == 0) {
+    for (int sl = 0; sl < 2; ++sl) {
+      mbar_init(BAR_A_READY(sl), N_EPI_WARPS);
+      mbar_init(BAR_ACC(sl), 1);
+    }
+    for (int st_ = 0; st_ < n_stages; ++st_) {
+      mbar_init(BAR_FULL(st_), 1);
+      mbar_init(BAR_EMPTY(st_), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t alo_base = smem_u32(alo);
+  const uint32_t st_base = smem_u32(stages);
+  const int pairs = umma::pp_pairs(F, op);
+
+  if (warp == 0) {
+    // ================================================= weight producer: each step once per slot
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+        int j0, j1, base, nv;
+        umma::pp_rows(F, op, pr, 0, j0, j1, base, nv);
+        for (int j = j0; j < j1; ++j) {
+          const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_x3);
+          const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+          const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
+          for (int s = 0; s < ns; ++s) {
+            const Step st = umma::load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            for (int sl = 0; sl < 2; ++sl) {
+              const uint8_t* src = img + st.img_off;
+              for (int kk = 0; kk < st.nchunk; ++kk) {
+                mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
+                mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
+                bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+                src += st.chunk_bytes;
+                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================= MMA issuer (whole warp, converged, uniform)
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t ar = 0u;
+    const uint32_t tmem_u = uni(tmem), bars_u = uni(bar0);
+    const uint32_t alo0_lo = uni(umma::sdesc_lo(alo_base)), w0_lo = uni(umma::sdesc_lo(st_base));
+    const uint32_t alo_step = uni((uint32_t)alo_bytes >> 4), sstep = uni((uint32_t)stage_bytes >> 4);
+    const int nst = uni(n_stages), pairs_u = uni(pairs);
+    for (int pr = blockIdx.x; pr < pairs_u; pr += gridDim.x) {
+      int j0, j1, base, nv;
+      umma::pp_rows(F, op, pr, 0, j0, j1, base, nv);
+      j0 = uni(j0);
+      j1 = uni(j1);
+      for (int j = j0; j < j1; ++j) {
+        const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_x3);
+        const int ns = uni(__ldg(Op::kGrad ? &P->n_grad : &P->n_fwd));
+        for (int s = 0; s < ns; ++s) {
+          Step st = umma::load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+          umma::uni_step(st);
+          const uint32_t id = idesc_tf32(st.N);
+          const uint32_t lo_off = (uint32_t)(st.N * 32) >> 4;   // W_lo block behind W_hi in a stage
+#pragma unroll
+          for (int sl = 0; sl < 2; ++sl) {
+            mbar_wait_u(bars_u + 8u * sl, ar & 1u);   // the slot's A (hi in TMEM, lo in shared memory)
+            tc_after_sync();
+            const uint32_t d_t = tmem_u + (uint32_t)(sl * 256 + (s & 1) * PP_REGION);
+            const uint32_t a_t = tmem_u + (uint32_t)(sl * 256 + ((s + 1) & 1) * PP_REGION);
+            const uint32_t alo_sl = alo0_lo + (uint32_t)sl * alo_step;
+            for (int kk = 0; kk < st.nchunk; ++kk) {
+              mbar_wait_u(bars_u + 8u * (uint32_t)(4 + stage), phase);
+              tc_after_sync();
+              const uint32_t bhi = w0_lo + (uint32_t)stage * sstep;
+              const uint32_t al = alo_sl + (uint32_t)(((kk >> 2) * ROWS * 128 + (kk & 3) * 32) >> 4);
+              mma_x3_step_w(d_t, a_t + (uint32_t)(kk * 8), bhi, bhi + lo_off, al, id, kk ? 1u : 0u,
+                            bars_u + 8u * (uint32_t)(4 + nst + stage));
+              if (++stage == nst) { stage = 0; phase ^= 1u; }
+            }
+            umma::tc_commit_w(bars_u + 8u * (uint32_t)(2 + sl));
+          }
+          ++ar;
+        }
+      }
+    }
+  } else {
+    // ================================================= row warps (both slots in turn)
+    const int q = warp & 3;
+    const int sub = (warp - EPI_WARP0) >> 2;   // column groups of this warp: g % 2 == sub
+    const int r = q * 32 + lane;
+    const int r7 = r & 7;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    uint32_t acc_ph[2] = {0u, 0u};
+    // this row of the next pair of tiles, fetched one pair ahead
+    int n_slot[2] = {0, 0};
+    double n_pos[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}}, n_u3[2] = {0.0, 0.0}, n_u4[2] = {0.0, 0.0};
+    auto fetch = [&](int pp) {
+      if (pp < pairs) {
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          int a0, a1, b0, c0;
+          umma::pp_rows(F, op, pp, sl, a0, a1, b0, c0);
+          if (r < c0) {
+            n_slot[sl] = op.slot(b0 + r);
+            if constexpr (!Op::kRaw) op.load(n_slot[sl], n_pos[sl], n_u3[sl], n_u4[sl]);
+          }
+        }
+      }
+    };
+    // a slot's A complete: TMEM stores done, shared stores visible to the async proxy
+    auto release = [&](int sl) {
+      tmem_wait_st();
+      tc_before_sync();
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(BAR_A_READY(sl));
+    };
+    fetch(blockIdx.x);
+    for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+      int j0 = 0, j1 = 0;
+      int slot_id[2] = {0, 0};
+      bool valid[2] = {false, false};
+      double pos[2][3], u3[2], u4[2], best[2] = {0.0, 0.0};
+      int bobj[2] = {0, 0};
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        int base, nv;
+        umma::pp_rows(F, op, pr, sl, j0, j1, base, nv);
+        valid[sl] = r < nv;
+        slot_id[sl] = valid[sl] ? n_slot[sl] : 0;
+        pos[sl][0] = n_pos[sl][0]; pos[sl][1] = n_pos[sl][1]; pos[sl][2] = n_pos[sl][2];
+        u3[sl] = n_u3[sl];
+        u4[sl] = n_u4[sl];
+      }
+      for (int j = j0; j < j1; ++j) {
+        const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_x3);
+        const NetDev& net = F.net[j];
+        const int head_off = __ldg(&P->head_off);
+        const int k0 = P->k0;
+        const bool pe = net.encoding == ENC_PE6;
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          {   // params of this network for the slot (the slot's previous network is done)
+            const int nf = __ldg(&P->params_floats);
+            const float4* src = reinterpret_cast<const float4*>(P->params);
+            float4* dst = reinterpret_cast<float4*>(sparams + sl * pfl);
+            named_sync(1, N_EPI_WARPS * 32);
+            for (int i = threadIdx.x - EPI_WARP0 * 32; i < (nf >> 2); i += N_EPI_WARPS * 32) dst[i] = __ldg(src + i);
+            named_sync(1, N_EPI_WARPS * 32);
+          }
+          // ---- input encoding -> A_hi (the slot's region 1) + A_lo, groups g % 2 == sub
+          const uint32_t enc_t = tmem + lane_addr + (uint32_t)(sl * 256 + PP_REGION);
+          const uint32_t alo_row = alo_base + (uint32_t)(sl * alo_bytes) + (uint32_t)((r >> 3) * 1024 + r7 * 128);
+          if constexpr (!Op::kRaw) {
+            double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            if (valid[sl]) row_u(F, j, pos[sl], u3[sl], u4[sl], u);
+            if (sub == 0) {
+              encode_group<0>(pe, valid[sl], u, enc_t, alo_row, r7);
+              if (k0 > 64) encode_group<2>(pe, valid[sl], u, enc_t + 64u, alo_row + 2u * ROWS * 128, r7);
+            } else if (k0 > 32) {
+              encode_group<1>(pe, valid[sl], u, enc_t + 32u, alo_row + 1u * ROWS * 128, r7);
+            }
+          } else {
+            for (int g = sub; g * 32 < k0; g += 2) {
+              float x[32];
+#pragma unroll
+              for (int e = 0; e < 32; ++e) x[e] = valid[sl] ? (float)op.raw(slot_id[sl], 32 * g + e) : 0.f;
+              put_group(x, enc_t + (uint32_t)(32 * g), alo_row + (uint32_t)(g * ROWS * 128), r7);
+            }
+          }
+          release(sl);
+        }
+        if (j == j0) fetch(pr + (int)gridDim.x);
+
+        const int ns = __ldg(Op::kGrad ? &P->n_grad : &P->n_fwd);
+        float head_part[2] = {0.f, 0.f};
+        for (int s = 0; s < ns; ++s) {
+          const Step st = umma::load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+          const int epi = st.epi;
+#pragma unroll
+          for (int sl = 0; sl < 2; ++sl) {
+            mbar_wait(BAR_ACC(sl), acc_ph[sl] & 1u);
+            ++acc_ph[sl];
+            tc_after_sync();
+            const uint32_t d_t = tmem + lane_addr + (uint32_t)(sl * 256 + (s & 1) * PP_REGION);
+            const uint32_t alo_row = alo_base + (uint32_t)(sl * alo_bytes) + (uint32_t)((r >> 3) * 1024 + r7 * 128);
+            uint32_t* my_masks = mask_scratch + ((size_t)blockIdx.x * 2 + sl) * MASK_WORDS_PER_CTA;
+            const float* sp = sparams + sl * pfl;
+            if (epi == E_BWD_OUT) {
+              if (sub == 0) {
+                float gin[96];
+#pragma unroll
+                for (int c = 0; c < 96; c += 16) {
+                  if (c < st.N) {
+                    uint32_t rg[16];
+                    DDF_TMEM_LD16(d_t + (uint32_t)c, rg);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) gin[c + e] = __uint_as_float(rg[e]);
+                  }
+                }
+                if constexpr (Op::kGrad) {
+                  if (valid[sl]) {
+                    if constexpr (Op::kRaw) {
+                      op.store_grad_raw(slot_id[sl], [&](int k) { return (double)gin[k]; });
+                    } else {
+                      double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+                      row_u(F, j, pos[sl], u3[sl], u4[sl], u);
+                      double g5[5];
+                      pe_chain(net, u, [&](int k) { return (double)gin[k]; }, g5);
+                      op.store_grad(slot_id[sl], g5);
+                    }
+                  }
+                }
+              }
+              tc_before_sync();
+              continue;
+            }
+            const int ng = (st.N + 31) >> 5;
+            const float* hw = sp + head_off;
+            for (int g = sub; g < PP_GROUPS; g += 2) {
+              if (g < ng) {
+                const int c = 32 * g;
+                const uint32_t tc = d_t + (uint32_t)c, al = alo_row + (uint32_t)(g * ROWS * 128);
+                switch (epi) {
+                  case E_RELU_A: epi_group<E_RELU_A>(st, c, r, tc, al, my_masks, hw, head_part[sl], sp); break;
+                  case E_RELU_MASK_A: epi_group<E_RELU_MASK_A>(st, c, r, tc, al, my_masks, hw, head_part[sl], sp); break;
+                  case E_MASKG_A: epi_group<E_MASKG_A>(st, c, r, tc, al, my_masks, hw, head_part[sl], sp); break;
+                  case E_BWD_MASK_A: epi_group<E_BWD_MASK_A>(st, c, r, tc, al, my_masks, hw, head_part[sl], sp); break;
+                  default: epi_group<E_HEAD>(st, c, r, tc, al, my_masks, hw, head_part[sl], sp); break;
+                }
+              }
+            }
+            if (epi != E_HEAD) {
+              release(sl);
+            } else {
+              tc_before_sync();
+              float* rd = red + sl * 2 * ROWS;
+              rd[sub * ROWS + r] = head_part[sl];
+              named_sync(1, N_EPI_WARPS * 32);
+              if (sub == 0) {
+                double pv = (double)(rd[r] + rd[ROWS + r] + P->head_b);
+                if (F.composite) pv = dmul(net.scale, pv);
+                if (j == j0 || pv < best[sl]) { best[sl] = pv; bobj[sl] = j; }
+              }
+              named_sync(1, N_EPI_WARPS * 32);
+            }
+          }
+        }
+      }
+      if constexpr (!Op::kGrad) {
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl)
+          if (sub == 0 && valid[sl]) op.store_fwd(slot_id[sl], best[sl], bobj[sl]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // ------------------------------------------------------------------ host side
 inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
 
@@ -717,6 +1027,25 @@ int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op,
     kmax = std::max(kmax, images[j].host.kmax);
     chunk = std::max(chunk, images[j].host.max_chunk_bytes);
     params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
+  }
+  int maxh = 0;
+  for (int j = 0; j < F.n_obj; ++j) maxh = std::max(maxh, images[j].host.max_hidden);
+  if (maxh <= PP_REGION && kmax <= PP_REGION) {
+    // two tiles per CTA in lock-step (mlp_x3pp_kernel)
+    const int alo_bytes = ROWS * pad_to(kmax, 32) * 4;
+    const int extra = 1024 /*align*/ + 8 * (4 + 2 * 12) + 16 + 4 * ROWS * 4 + 2 * params_bytes;
+    const int n_stages = std::min(12, (umma::SMEM_LIMIT - 2 * alo_bytes - extra) / chunk);
+    if (n_stages < 2) { *err = "3xTF32 two-tile engine: not enough shared memory for the weight pipeline"; return 1; }
+    const size_t smem = 2 * (size_t)alo_bytes + (size_t)n_stages * chunk + extra;
+    auto kern = mlp_x3pp_kernel<Op>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) { *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e); return 4; }
+    const int pairs_max = ((max_rows + ROWS - 1) / ROWS + 1) / 2 + (Op::kGrad ? F.n_obj : 0);
+    const int grid = std::max(1, std::min(pairs_max, sm_count));
+    kern<<<grid, NTHREADS, smem, st>>>(F, op, mask_scratch, n_stages, alo_bytes, chunk, params_bytes);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { *err = std::string("mlp_x3pp_kernel launch: ") + cudaGetErrorString(e); return 4; }
+    return 0;
   }
   const int alo_bytes = ROWS * pad_to(kmax, 32) * 4;
   const int extra = 1024 /*align*/ + 8 * (GROUPS + 2 + 2 * 12) + 16 + 2 * ROWS * 4 + params_bytes;
