@@ -384,6 +384,11 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
   const int r7 = r & 7;
   uint32_t hold[HOLD > 0 ? HOLD : 1][16];
   auto store = [&](int c, const uint32_t* pk) {
+#ifdef DDF_EXP_NOST
+    // timing experiment only (wrong results): no A-tile stores, what do they cost the MMAs beside them?
+    if (pk[0] == 0x12345678u && pk[7] == 0x9abcdef0u) st_shared_v4(a_row, pk[0], pk[1], pk[2], pk[3]);
+    return;
+#endif
     // 4 x 16 B of one row into the 128B-swizzled A tile (row base a_row)
     const uint32_t blk = a_row + (uint32_t)((c >> 6) * (ROWS * 128));
     const int cc0 = (c & 63) >> 3;
@@ -497,6 +502,13 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
   // alternating with them).  tcgen05.wait::ld waits for every outstanding
   // load, hence one chunk of look-ahead.
   uint32_t rg[2][32];
+#ifdef DDF_EXP_NOLD
+  // timing experiment only (wrong results): no accumulator loads, what does the TMEM read port cost?
+#pragma unroll
+  for (int e = 0; e < 32; ++e) { rg[0][e] = (uint32_t)(r * 977 + e); rg[1][e] = (uint32_t)(r * 131 + e); }
+#undef DDF_TMEM_LD32
+#define DDF_TMEM_LD32(taddr, r_) ((void)0)
+#endif
   if constexpr (NM > 0) {
     DDF_TMEM_LD32(tmem_row + (uint32_t)c_first, rg[0]);
     tmem_wait_ld();
