@@ -134,6 +134,17 @@ __device__ __forceinline__ void uni_step(Step& st) {
   st.nchunk = uni(st.nchunk); st.rows = uni(st.rows);
 }
 
+// Bias folded into the accumulator (ping-pong and quad programs, hidden widths
+// <= 256).  The epilogue's shared-memory traffic competes with the MMAs'
+// operand fetch (profiles/r2_exp_epilogue_cost.txt), and a third of it was
+// the broadcast bias loads.  Each forward-type step of these programs carries
+// one more weight chunk whose K columns 0..2 hold the bias split into three
+// bf16 pieces (hi + mid + lo = the fp32 bias to ~2^-24), and the issuer adds
+// one K = 16 MMA of it against a constant A block whose columns 0..2 are 1:
+// D += 1 * b_hi + 1 * b_mid + 1 * b_lo.  The epilogue then reads z, not z - b.
+__host__ __device__ inline bool step_has_bias(int epi) {
+  return epi == E_RELU_A || epi == E_HEAD || epi == E_RELU_MASK_A || epi == E_MASKG_A;
+}
 struct Prog {
   int n_fwd, n_grad;
   int k0;              // padded input width (multiple of 16)
@@ -143,6 +154,7 @@ struct Prog {
   int max_chunk_bytes;
   int pp;              // 1: two-tile ping-pong program (hidden widths <= 256, one N-half per step)
   int max_hidden;      // widest padded hidden layer (<= 128: four-slot quad kernel)
+  int fold;            // 1: forward-type steps carry a bias chunk after their K chunks (pp / quad programs)
   float head_b;
   const float* head_w; // fp32, padded last hidden width
   const float* params; // fp32 block: hidden-layer biases then head weights (staged in shared memory)
@@ -270,6 +282,30 @@ __device__ __forceinline__ void mma_k64_commit(uint32_t tmem_d, uint64_t da, uin
 // operand here, so the K-step advances are 32-bit adds.
 constexpr uint32_t SDESC_HI = (uint32_t)((1024 >> 4) | (1u << 14) | (2u << 29));
 __device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr) { return ((saddr & 0x3FFFFu) >> 4) | (1u << 16); }
+// The constant A block: 128 rows x 32 B, 32-byte swizzle (16-byte half h of
+// row r at h ^ ((r >> 2) & 1)), columns 0..2 = 1.0 bf16, the rest 0.
+constexpr int ONES_BYTES = ROWS * 32;
+constexpr uint32_t SDESC32B_HI = (uint32_t)((256 >> 4) | (1u << 14) | (6u << 29));   // SBO 256 B, version, SWIZZLE_32B
+__device__ __forceinline__ void write_ones_block(uint8_t* ones, int tid, int nthreads) {
+  for (int r = tid; r < ROWS; r += nthreads) {
+    uint4* row = reinterpret_cast<uint4*>(ones + r * 32);
+    const int h0 = (r >> 2) & 1;
+    row[h0] = make_uint4(0x3F803F80u, 0x00003F80u, 0u, 0u);   // bf16 1, 1, 1, 0, 0, 0, 0, 0
+    row[h0 ^ 1] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+// the fold's MMA: A = the ones block, B = the bias chunk (both one K = 16 step, 32-byte swizzle)
+__device__ __forceinline__ void mma_bias_w(uint32_t tmem_d, uint32_t ones_lo, uint32_t db_lo, uint32_t id) {
+  asm volatile(
+      "{\n\t.reg .pred q, e;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.b32 q, %3, %3;\n\t"
+      "mov.b64 a, {%1, %4};\n\tmov.b64 b, {%2, %4};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t}" ::"r"(tmem_d),
+      "r"(ones_lo), "r"(db_lo), "r"(id), "n"(SDESC32B_HI)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_k64_commit_w(uint32_t tmem_d, uint32_t da, uint32_t db, uint32_t id,
                                                  uint32_t acc, uint32_t bar) {
   asm volatile(
@@ -1547,7 +1583,7 @@ __device__ __forceinline__ void epi_cols16(const Step& st, int c_first, int r, u
   constexpr bool WA = EPI != E_HEAD;
   constexpr bool HEAD_DOT = EPI == E_HEAD || EPI == E_MASKG_HEAD_A;
   const int r7 = r & 7;
-  const uint32_t bias_s = smem_u32(sparams) + 4u * (uint32_t)(size_t)st.bias;
+  (void)sparams;
   const uint32_t head_s = smem_u32(head_w);
   uint32_t rg[2][16];
   uint32_t mw = 0u, mq = 0u;
@@ -1561,14 +1597,10 @@ __device__ __forceinline__ void epi_cols16(const Step& st, int c_first, int r, u
     if (i + 1 < 2 * NM)
       DDF_TMEM_LD16(tmem_row + (uint32_t)(c_first + ((i + 1) >> 1) * STRIDE + ((i + 1) & 1) * 16), rg[(i + 1) & 1]);
     const uint32_t(&x)[16] = rg[i & 1];
-    float4 bq[4];
-    if constexpr (EPI != E_BWD_MASK_A) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) bq[k] = ld_shared_f4(bias_s + 4u * (uint32_t)(c + 4 * k));
-    } else if ((i & 1) == 0) {
-      mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
+    // no bias here: it is already in the accumulator (step_has_bias)
+    if constexpr (EPI == E_BWD_MASK_A) {
+      if ((i & 1) == 0) mq = my_masks[(st.mask_layer * 16 + (c >> 5)) * ROWS + r];
     }
-    const float* bf = reinterpret_cast<const float*>(bq);
     uint32_t pkd[8];
     if constexpr (EPI == E_BWD_MASK_A) {
       const uint32_t m = mq >> (16 * (i & 1));
@@ -1579,15 +1611,15 @@ __device__ __forceinline__ void epi_cols16(const Step& st, int c_first, int r, u
     } else if constexpr (EPI == E_RELU_A) {
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        pkd[e] = pack_bf16_relu(__uint_as_float(x[2 * e]) + bf[2 * e], __uint_as_float(x[2 * e + 1]) + bf[2 * e + 1]);
+        pkd[e] = pack_bf16_relu(__uint_as_float(x[2 * e]), __uint_as_float(x[2 * e + 1]));
     } else if constexpr (EPI == E_HEAD) {
 #pragma unroll
       for (int e = 0; e < 16; e += 4) {
         const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
-        head_part = fmaf(fmaxf(__uint_as_float(x[e]) + bf[e], 0.f), hw.x, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(x[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(x[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(x[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(x[e]), 0.f), hw.x, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(x[e + 1]), 0.f), hw.y, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(x[e + 2]), 0.f), hw.z, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(x[e + 3]), 0.f), hw.w, head_part);
       }
     } else {
       // ReLU mask bits (neural.py:241 "h > 0"), one u32 per 32 columns
@@ -1595,7 +1627,7 @@ __device__ __forceinline__ void epi_cols16(const Step& st, int c_first, int r, u
       float v[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const float z = __uint_as_float(x[e]) + bf[e];
+        const float z = __uint_as_float(x[e]);
         mh |= (z > 0.f ? 1u : 0u) << e;
         v[e] = z;
       }
@@ -1680,7 +1712,8 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)n_stages * stage_bytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSL + 2 * n_stages);
   float* sparams = reinterpret_cast<float*>(tmem_slot + 4);      // one copy: [params_bytes/4]
-  (void)params_bytes;
+  // the bias fold's constant A block, aligned to its 256-byte swizzle atom
+  uint8_t* ones = reinterpret_cast<uint8_t*>(((uintptr_t)(sparams + (params_bytes >> 2)) + 255) & ~(uintptr_t)255);
 
   const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t bar0 = smem_u32(bars);
@@ -1704,6 +1737,8 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  write_ones_block(ones, threadIdx.x, blockDim.x);
+  fence_async_smem();
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
@@ -1729,13 +1764,15 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
           const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
           for (int s = 0; s < ns; ++s) {
             const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
-            for (int c = 0; c < st.nchunk; ++c) {
+            const int nck = st.nchunk + (step_has_bias(st.epi) ? 1 : 0);   // + the bias chunk (rows x 32 B)
+            for (int c = 0; c < nck; ++c) {
               const uint8_t* src = img + st.img_off + (size_t)c * st.chunk_bytes;
+              const uint32_t bytes = c < st.nchunk ? (uint32_t)st.chunk_bytes : (uint32_t)(st.rows * 32);
               DDF_DBG_T0();
               mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
               DDF_DBG_ADD(6);
-              mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
-              bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+              mbar_expect_tx(BAR_FULL(stage), bytes);
+              bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, bytes, BAR_FULL(stage));
               if (++stage == n_stages) { stage = 0; phase ^= 1u; }
             }
           }
@@ -1762,6 +1799,7 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
       const uint32_t a_step = uni((uint32_t)a_bytes >> 4), sstep = uni((uint32_t)stage_bytes >> 4);
       const uint32_t bars_u = uni(bar0);
       const int nst = uni(n_stages), packs_u = uni(packs);
+      const uint32_t ones_lo = uni(sdesc_lo(smem_u32(ones)));
       TraceCursor tcur{1, 0};
       for (int pk = blockIdx.x; pk < packs_u; pk += gridDim.x) {
         int j0, j1, base, nv;
@@ -1812,11 +1850,19 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
                 }
                 if (++stg == nst) { stg = 0; ph ^= 1u; }
               }
+              if (step_has_bias(st.epi)) {   // D += bias: the chunk after the K chunks, shared by the slots
+                if (sl == 0) {
+                  mbar_wait_u(bars_u + 8u * (uint32_t)(2 * NSL + stg), ph);
+                  tc_after_sync();
+                }
+                mma_bias_w(td, ones_lo, db0_lo + (uint32_t)stg * sstep, id);
+              }
               tc_commit_w(bars_u + 8u * (uint32_t)(NSL + sl));
               tcur.ev(trc, 7, s * NSL + sl, 0);              // 7: the slot's layer issued
             }
             ++ar;
-            for (int kc = 0; kc < st.nchunk; ++kc) {     // every slot has read the layer's chunks
+            const int nck = st.nchunk + (step_has_bias(st.epi) ? 1 : 0);
+            for (int kc = 0; kc < nck; ++kc) {           // every slot has read the layer's chunks
               tc_commit_w(bars_u + 8u * (uint32_t)(2 * NSL + nst + stage));
               if (++stage == nst) { stage = 0; phase ^= 1u; }
             }
@@ -2042,6 +2088,25 @@ inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src) {
     }
 }
 
+// The bias chunk of a folded step (see step_has_bias): rows x 16 bf16 (one
+// K = 16 step, 32 B per row, 32-byte swizzle: 16-byte half h of row n at
+// h ^ ((n >> 2) & 1)), columns 0..2 of row n = the three bf16 pieces of
+// bias[n].  It follows the step's K chunks in the image.
+inline int bias_chunk_bytes(int rows) { return rows * 32; }
+inline void append_bias_chunk(std::vector<uint16_t>& img, const Step& st, const std::vector<float>& bias) {
+  const size_t base = img.size();
+  img.resize(base + (size_t)st.rows * 16, 0);
+  for (int n = 0; n < st.rows; ++n) {
+    float rem = bias[n];
+    for (int k = 0; k < 3; ++k) {
+      const __nv_bfloat16 b = __float2bfloat16_rn(rem);
+      rem -= __bfloat162float(b);
+      const size_t off = (size_t)n * 16 + (size_t)((((k >> 3) ^ ((n >> 2) & 1)) << 3) + (k & 7));
+      std::memcpy(&img[base + off], &b, 2);
+    }
+  }
+}
+
 inline Step make_step(int K, int N, int nh, int epi) {
   Step s{};
   s.K = K; s.N = N; s.nh = nh; s.epi = epi;
@@ -2087,6 +2152,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   Prog& P = out->host;
   std::memset(&P, 0, sizeof(P));
   P.pp = split == 1;
+  P.fold = maxh <= 128;   // quad programs
   P.max_hidden = maxh;
   P.k0 = wp[0];
   P.in_width = widths[0];
@@ -2108,6 +2174,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
     const std::vector<float>& w = W[l];
     const int K = wp[l];
     append_chunks(img, s, [&](int n, int k) { return w[(size_t)n * K + k]; });
+    if (P.fold) append_bias_chunk(img, s, B[l]);
     s.bias = reinterpret_cast<const float*>(bias_off[l]);   // patched to device below
     P.fwd[l] = s;
   }
@@ -2120,6 +2187,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
     const std::vector<float>& w = W[l];
     const int K = wp[l];
     append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)n * K + k]; });
+    if (P.fold) append_bias_chunk(gimg, s, B[l]);
     s.bias = reinterpret_cast<const float*>(bias_off[l]);
     P.grad[gs++] = s;
   }
@@ -2211,7 +2279,7 @@ int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op
     params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
   }
   const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
-  const int extra = 1024 + 8 * (2 * NSL + 2 * 8) + 16 + params_bytes;
+  const int extra = 1024 + 8 * (2 * NSL + 2 * 8) + 16 + params_bytes + ONES_BYTES + 256;
   int n_stages = std::min(8, (SMEM_LIMIT - NSL * a_bytes - extra) / chunk);
   if (n_stages < 2) { *err = "bf16 quad engine: not enough shared memory"; return 1; }
   const size_t smem = NSL * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
@@ -2230,7 +2298,6 @@ int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op
 template <class Op>
 int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op, int max_rows, int sm_count,
            uint32_t* mask_scratch, cudaStream_t st, std::string* err) {
-  const int dbgq = debug_bits();
   int maxh = 0;
   bool all_pp = true;
   for (int j = 0; j < F.n_obj; ++j) {
@@ -2240,12 +2307,13 @@ int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op,
   // <= 128 wide: four slots, one row-warp group per slot.  129..256 wide: the
   // ping-pong engine below (a two-slot group-per-slot variant measured slower:
   // 880 vs 1065 TF/s forward on 5->8x256, c5 60.1 M vs 69.6 M path samples/s).
-  // dbg 512 forces the ping-pong engine (A/B timing).
+  // Quad programs carry folded bias chunks (step_has_bias), which only the
+  // quad kernel consumes.
   if constexpr (Op::kFused) {
     // fused trace+gradient exists for the > 256-wide single-tile engine only
     if (all_pp || F.n_obj != 1) { *err = "fused trace+gradient needs one network wider than 256"; return 1; }
   } else {
-  if (all_pp && maxh <= 128 && !(dbgq & 512))
+  if (all_pp && maxh <= 128)
     return launch_quad<Op, 4>(F, images, op, max_rows, sm_count, mask_scratch, st, err);
   bool pp = true, any_pp = false;
   for (int j = 0; j < F.n_obj; ++j) {
