@@ -478,7 +478,7 @@ def bench_bvh(args, rank, world, local):
     res = {"metric": "path_samples_per_s", "value": samples / (ms / 1e3), "unit": "path_samples/s", "n_gpus": world,
            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "bvh", "mesh": "blob(4, 0)", "triangles": int(m.n_faces), "W": cam.width,
+           "config": {"workload": "bvh", "mesh": "blob(4, 0)", "triangles": int(len(reference_mesh()[1])), "W": cam.width,
                       "H": cam.height, "spp": cfg.spp, "bounces": cfg.bounces,
                       "l2": "flushed (256 MB write) between timed steps"},
            "roofline": {"bound": "fp64", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
