@@ -104,6 +104,18 @@ __device__ __forceinline__ void mma2_bf16_w(uint32_t tmem_d, uint32_t da, uint32
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, p;\n\t}" ::"r"(tmem_d),
       "r"(da), "r"(db), "r"(id), "r"(acc), "n"(SDESC_HI));
 }
+// the bias fold's MMA for the pair (see mlp_umma.cuh step_has_bias): A = each CTA's ones block,
+// B = each CTA's half of the bias chunk, both one K = 16 step in the 32-byte swizzle
+__device__ __forceinline__ void mma2_bias_w(uint32_t tmem_d, uint32_t ones_lo, uint32_t db_lo, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred q, e;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %4, 0;\n\t"
+      "mov.b64 a, {%1, %5};\n\tmov.b64 b, {%2, %5};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, q;\n\t}" ::"r"(tmem_d),
+      "r"(ones_lo), "r"(db_lo), "r"(id), "r"(acc), "n"(SDESC32B_HI)
+      : "memory");
+}
 // MMA completion -> the barrier at this offset in BOTH CTAs of the pair
 __device__ __forceinline__ void tc_commit2_w(uint32_t bar) {
   asm volatile(
@@ -138,6 +150,8 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
   S.tmem_slot = reinterpret_cast<uint32_t*>(S.bars + 6 + 2 * n_stages);
   S.red = reinterpret_cast<float*>(S.tmem_slot + 4);
   S.params = S.red + 2 * ROWS;
+  // the bias fold's constant A block, aligned to its 256-byte swizzle atom
+  uint8_t* ones = reinterpret_cast<uint8_t*>(((uintptr_t)(S.params + (params_bytes >> 2)) + 255) & ~(uintptr_t)255);
 
   const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t rank = cluster_ctarank();
@@ -165,6 +179,8 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(S.tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
+  write_ones_block(ones, threadIdx.x, blockDim.x);
+  fence_async_smem();
   tc_before_sync();
   cluster_sync_all();   // both CTAs' barriers initialised before any remote arrive or multicast commit
   tc_after_sync();
@@ -192,18 +208,32 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
           for (int s = 0; s < ns; ++s) {
             const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
             const int half_rows = st.rows >> 1;
+            const bool fold = step_has_bias(st.epi);   // a bias chunk (rows x 32 B) ahead of each N-half
             // this CTA's half of every chunk: rows [rank * half, (rank + 1) * half)
-            int row = img_row0 + (int)(st.img_off >> 7) + (int)rank * half_rows;
-            const int nck = st.nh * st.nchunk;
-            for (int c = 0; c < nck; ++c) {
-              mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
-              const uint32_t dst = st_base + (uint32_t)(stage * stage_bytes);
-              if (rank == 0) mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);   // both halves
-              int r0 = 0;
-              for (; r0 + 128 <= half_rows; r0 += 128) tma_box_pair(dst + (uint32_t)(r0 * 128), &tm.box128, row + r0, BAR_FULL(stage));
-              for (; r0 < half_rows; r0 += 8) tma_box_pair(dst + (uint32_t)(r0 * 128), &tm.box8, row + r0, BAR_FULL(stage));
-              row += st.rows;
-              if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+            int base_row = img_row0 + (int)(st.img_off >> 7);   // in rows of 128 bytes
+            for (int h = 0; h < st.nh; ++h) {
+              if (fold) {
+                mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
+                const uint32_t dst = st_base + (uint32_t)(stage * stage_bytes);
+                if (rank == 0) mbar_expect_tx(BAR_FULL(stage), (uint32_t)(st.rows * 32));   // both halves
+                const int row32 = 4 * base_row + (int)rank * half_rows;                      // in rows of 32 bytes
+                int r0 = 0;
+                for (; r0 + 128 <= half_rows; r0 += 128) tma_box_pair(dst + (uint32_t)(r0 * 32), &tm.b32_128, row32 + r0, BAR_FULL(stage));
+                for (; r0 < half_rows; r0 += 8) tma_box_pair(dst + (uint32_t)(r0 * 32), &tm.b32_8, row32 + r0, BAR_FULL(stage));
+                base_row += st.rows >> 2;
+                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              }
+              for (int c = 0; c < st.nchunk; ++c) {
+                mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
+                const uint32_t dst = st_base + (uint32_t)(stage * stage_bytes);
+                if (rank == 0) mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);   // both halves
+                const int row = base_row + (int)rank * half_rows;
+                int r0 = 0;
+                for (; r0 + 128 <= half_rows; r0 += 128) tma_box_pair(dst + (uint32_t)(r0 * 128), &tm.box128, row + r0, BAR_FULL(stage));
+                for (; r0 < half_rows; r0 += 8) tma_box_pair(dst + (uint32_t)(r0 * 128), &tm.box8, row + r0, BAR_FULL(stage));
+                base_row += st.rows;
+                if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+              }
             }
           }
         }
@@ -222,6 +252,7 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
       const uint32_t tmem_u = uni(tmem), bars_u = uni(bar0);
       const uint32_t da0_lo = uni(sdesc_lo(a_base)), db0_lo = uni(sdesc_lo(st_base));
       const uint32_t sstep = uni((uint32_t)stage_bytes >> 4);
+      const uint32_t ones_lo = uni(sdesc_lo(smem_u32(ones)));
       const int nst = uni(n_stages), pairs_u = uni(pairs_total);
       auto UB_A_READY = [&](int h) { return bars_u + 8u * (0 + h); };
       auto UB_ACC = [&](int h) { return bars_u + 8u * (2 + h); };
@@ -244,6 +275,7 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
             uni_step(st);
             const uint32_t id = idesc2(st.rows);
             const bool wa = writes_a(st.epi);
+            const bool fold = step_has_bias(st.epi);
             const int kc1 = min(st.nchunk, (st.K >> 1) >> 6);
             const int c0 = min(st.nchunk - 1, ((st.N >> 1) - 1) >> 6);
             const int nfull = st.K >> 6;
@@ -263,6 +295,14 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
               while (kc < st.nchunk) {
                 if (kc == 0 && !waited0) { wait_a(0); waited0 = true; }
                 if (kc >= kc1 && !waited1) { wait_a(1); waited1 = true; }
+                if (kc == 0 && fold) {
+                  // the half's accumulator starts as its bias (ones block x bias chunk), the K chunks add to it
+                  mbar_wait_u(UB_FULL(stage), phase);
+                  tc_after_sync();
+                  mma2_bias_w(td, ones_lo, db0_lo + (uint32_t)stage * sstep, id, 0u);
+                  tc_commit2_w(UB_EMPTY(stage));
+                  if (++stage == nst) { stage = 0; phase ^= 1u; }
+                }
                 int kend = st.nchunk;
                 if (!waited1 && kc1 > kc) kend = min(kend, kc1);
                 if (wa && last_half && c0 >= kc) kend = min(kend, c0 + 1);
@@ -272,7 +312,7 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
                   mbar_wait_u(UB_FULL(stage), phase);
                   tc_after_sync();
                   mma2_k64_commit_w(td, da0_lo + (uint32_t)(kc * (ROWS * 128 / 16)), db0_lo + (uint32_t)stage * sstep,
-                                    id, kc ? 1u : 0u, UB_EMPTY(stage));
+                                    id, (kc || fold) ? 1u : 0u, UB_EMPTY(stage));
                   tcur.ev(trc, 8, s, h);
                   if (++stage == nst) { stage = 0; phase ^= 1u; }
                 }
@@ -282,7 +322,7 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
                   const int nks = (st.K - kc * 64 + 15) >> 4;
                   const uint32_t da = da0_lo + (uint32_t)(kc * (ROWS * 128 / 16));
                   const uint32_t db = db0_lo + (uint32_t)stage * sstep;
-                  for (int ks = 0; ks < nks; ++ks) mma2_bf16_w(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
+                  for (int ks = 0; ks < nks; ++ks) mma2_bf16_w(td, da + 2 * ks, db + 2 * ks, id, (kc | ks || fold) ? 1u : 0u);
                   tc_commit2_w(UB_EMPTY(stage));
                   if (++stage == nst) { stage = 0; phase ^= 1u; }
                   ++kc;
@@ -439,22 +479,22 @@ mlp2_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, 
             const long long t_epi = kStats ? clock64() : 0;
             switch (epi) {
               case E_RELU_A:
-                epi_half<E_RELU_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_RELU_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_RELU_MASK_A:
-                epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_RELU_MASK_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_MASKG_A:
                 if constexpr (Op::kFused)
-                  epi_half<E_MASKG_HEAD_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                  epi_half<E_MASKG_HEAD_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 else
-                epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_MASKG_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_BWD_MASK_A:
-                epi_half<E_BWD_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_BWD_MASK_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               default:
-                epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_HEAD, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
             }
             if (kStats && threadIdx.x == EPI_WARP0 * 32) dbg_acc[7] += (unsigned long long)(clock64() - t_epi);
@@ -503,7 +543,7 @@ int launch_2sm(const FieldDev& F, const NetImage& im, const Op& op, int max_rows
   const int a_bytes = ROWS * pad_to(im.host.kmax, 64) * 2;
   const int params_bytes = im.host.params_floats * 4;
   const int stage_bytes = 16384;
-  const int extra = 1024 /*align*/ + 8 * (6 + 2 * 8) + 16 + 2 * ROWS * 4 + params_bytes;
+  const int extra = 1024 /*align*/ + 8 * (6 + 2 * 8) + 16 + 2 * ROWS * 4 + params_bytes + ONES_BYTES + 256;
   const int n_stages = std::min(8, (SMEM_LIMIT - a_bytes - extra) / stage_bytes);
   if (n_stages < 2) { *err = "bf16 pair engine: not enough shared memory for the weight pipeline"; return 1; }
   const size_t smem = (size_t)a_bytes + (size_t)n_stages * stage_bytes + extra;

@@ -295,14 +295,15 @@ __device__ __forceinline__ void write_ones_block(uint8_t* ones, int tid, int nth
   }
 }
 // the fold's MMA: A = the ones block, B = the bias chunk (both one K = 16 step, 32-byte swizzle)
-__device__ __forceinline__ void mma_bias_w(uint32_t tmem_d, uint32_t ones_lo, uint32_t db_lo, uint32_t id) {
+__device__ __forceinline__ void mma_bias_w(uint32_t tmem_d, uint32_t ones_lo, uint32_t db_lo, uint32_t id,
+                                           uint32_t acc = 1u) {
   asm volatile(
       "{\n\t.reg .pred q, e;\n\t.reg .b64 a, b;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.eq.b32 q, %3, %3;\n\t"
-      "mov.b64 a, {%1, %4};\n\tmov.b64 b, {%2, %4};\n\t"
+      "setp.ne.b32 q, %4, 0;\n\t"
+      "mov.b64 a, {%1, %5};\n\tmov.b64 b, {%2, %5};\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t}" ::"r"(tmem_d),
-      "r"(ones_lo), "r"(db_lo), "r"(id), "n"(SDESC32B_HI)
+      "r"(ones_lo), "r"(db_lo), "r"(id), "r"(acc), "n"(SDESC32B_HI)
       : "memory");
 }
 
@@ -408,14 +409,14 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 // first two packed chunks are held until the A columns are free (a_free),
 // later chunks store directly.  Specialised per epilogue kind and chunk count
 // so each fully unrolled loop carries only the arithmetic it needs.
-template <int EPI, int NM>
+template <int EPI, int NM, bool FOLD = false>
 __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, uint32_t tmem_row, uint32_t a_row,
                                            uint32_t* my_masks, const float* head_w, float& head_part,
                                            uint32_t bar_free, uint32_t& free_ph, const float* sparams,
                                            const uint32_t (&mpre)[4]) {
   constexpr bool WA = EPI == E_RELU_A || EPI == E_RELU_MASK_A || EPI == E_MASKG_A || EPI == E_BWD_MASK_A ||
                      EPI == E_MASKG_HEAD_A;
-  constexpr bool BIAS = EPI != E_BWD_MASK_A;
+  constexpr bool BIAS = EPI != E_BWD_MASK_A && !FOLD;   // FOLD: the bias is already in the accumulator
   constexpr int HOLD = NM < 2 ? NM : 2;
   const int r7 = r & 7;
   uint32_t hold[HOLD > 0 ? HOLD : 1][16];
@@ -454,12 +455,13 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
     (void)b;
     return __uint_as_float(acc);
 #else
-    return __uint_as_float(acc) + b;
+    if constexpr (FOLD) return __uint_as_float(acc);
+    else return __uint_as_float(acc) + b;
 #endif
   };
   auto proc = [&](const int i, const int c, const uint32_t (&rg)[32], const float4 (&bq)[8]) {
       uint32_t mq = 0u;
-      if constexpr (!BIAS) mq = mpre[i];   // prefetched before the accumulator wait
+      if constexpr (EPI == E_BWD_MASK_A) mq = mpre[i];   // prefetched before the accumulator wait
       const float* bf = reinterpret_cast<const float*>(bq);
       uint32_t pkd[16];
       if constexpr (EPI == E_BWD_MASK_A) {
@@ -560,17 +562,17 @@ __device__ __forceinline__ void epi_chunks(const Step& st, int c_first, int r, u
   if constexpr (WA && NM == 0) ++free_ph;   // no columns in this half: keep the phase count in step
 }
 
-template <int EPI>
+template <int EPI, bool FOLD = false>
 __device__ __forceinline__ void epi_half(int nmine, const Step& st, int c_first, int r, uint32_t tmem_row,
                                          uint32_t a_row, uint32_t* my_masks, const float* head_w, float& head_part,
                                          uint32_t bar_free, uint32_t& free_ph, const float* sp,
                                          const uint32_t (&mpre)[4]) {
   switch (nmine) {
-    case 0: epi_chunks<EPI, 0>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
-    case 1: epi_chunks<EPI, 1>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
-    case 2: epi_chunks<EPI, 2>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
-    case 3: epi_chunks<EPI, 3>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
-    default: epi_chunks<EPI, 4>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    case 0: epi_chunks<EPI, 0, FOLD>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    case 1: epi_chunks<EPI, 1, FOLD>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    case 2: epi_chunks<EPI, 2, FOLD>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    case 3: epi_chunks<EPI, 3, FOLD>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
+    default: epi_chunks<EPI, 4, FOLD>(st, c_first, r, tmem_row, a_row, my_masks, head_w, head_part, bar_free, free_ph, sp, mpre); break;
   }
 }
 
@@ -720,6 +722,8 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
   S.tmem_slot = reinterpret_cast<uint32_t*>(S.bars + 6 + 2 * n_stages);
   S.red = reinterpret_cast<float*>(S.tmem_slot + 4);
   S.params = S.red + 2 * ROWS;
+  // the bias fold's constant A block (step_has_bias), aligned to its 256-byte swizzle atom
+  uint8_t* ones = reinterpret_cast<uint8_t*>(((uintptr_t)(S.params + (params_bytes >> 2)) + 255) & ~(uintptr_t)255);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(S.bars);
@@ -745,6 +749,8 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(S.tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  write_ones_block(ones, threadIdx.x, blockDim.x);
+  fence_async_smem();
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
@@ -772,8 +778,11 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
           for (int s = 0; s < ns; ++s) {
             const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
             const uint8_t* src = img + st.img_off;
-            const int nck = st.nh * st.nchunk;
+            const bool fold = step_has_bias(st.epi);   // wide programs carry a bias chunk ahead of each N-half
+            const int per_half = st.nchunk + (fold ? 1 : 0);
+            const int nck = st.nh * per_half;
             for (int c = 0; c < nck; ++c) {
+              const uint32_t bytes = (fold && c % per_half == 0) ? (uint32_t)(st.rows * 32) : (uint32_t)st.chunk_bytes;
               {
                 DDF_DBG_T0();
                 mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
@@ -782,10 +791,10 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
               if (dbg & 1) {   // timing experiment only: no weight traffic (wrong results)
                 mbar_arrive(BAR_FULL(stage));
               } else {
-                mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
-                bulk_g2s(st_base + (uint32_t)(stage * sstride), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+                mbar_expect_tx(BAR_FULL(stage), bytes);
+                bulk_g2s(st_base + (uint32_t)(stage * sstride), src, bytes, BAR_FULL(stage));
               }
-              src += st.chunk_bytes;
+              src += bytes;
               if (++stage == n_stages) { stage = 0; phase ^= 1u; }
             }
           }
@@ -809,6 +818,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
       const uint64_t da0 = sdesc(a_base), db0 = sdesc(st_base);
       const uint32_t da0_lo = sdesc_lo(a_base), db0_lo = sdesc_lo(st_base);
       const uint32_t sstep = (uint32_t)sstride >> 4;
+      const uint32_t ones_lo = sdesc_lo(smem_u32(ones));
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         int j0, j1, base, nv;
         tile_rows(F, op, t, j0, j1, base, nv);
@@ -823,6 +833,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
             const Step st = load_step(kProgG ? &P->grad[s] : &P->fwd[s]);
             const uint32_t id = idesc(st.rows);
             const bool wa = writes_a(st.epi);
+            const bool fold = step_has_bias(st.epi);
             // chunks [0, kc1) read A columns < K/2 (A_READY(0)), the rest also
             // columns >= K/2 (A_READY(1)); in the last N-half, A_FREE(0) follows
             // chunk c0 (the last reading A columns < N/2) and A_FREE(1) the last
@@ -854,6 +865,14 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
               while (kc < st.nchunk) {
                 if (kc == 0 && !waited0) { wait_a(0); waited0 = true; }
                 if (kc >= kc1 && !waited1) { wait_a(1); waited1 = true; }
+                if (kc == 0 && fold) {
+                  // the half's accumulator starts as its bias (ones block x bias chunk), the K chunks add to it
+                  mbar_wait(BAR_FULL(stage), phase);
+                  tc_after_sync();
+                  mma_bias_w(td, ones_lo, db0_lo + (uint32_t)stage * sstep, id, 0u);
+                  tc_commit_w(BAR_EMPTY(stage));
+                  if (++stage == n_stages) { stage = 0; phase ^= 1u; }
+                }
                 int kend = st.nchunk;
                 if (!waited1 && kc1 > kc) kend = min(kend, kc1);
                 if (wa && last_half && c0 >= kc) kend = min(kend, c0 + 1);
@@ -866,7 +885,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                     tc_commit_w(BAR_EMPTY(stage));
                   } else {
                     mma_k64_commit_w(td, da0_lo + (uint32_t)(kc * (ROWS * 128 / 16)), db0_lo + (uint32_t)stage * sstep,
-                                     id, kc ? 1u : 0u, BAR_EMPTY(stage));
+                                     id, (kc || fold) ? 1u : 0u, BAR_EMPTY(stage));
                   }
                   tcur.ev(trc, 8, s, h);                  // 8: K chunk issued
                   if (++stage == n_stages) { stage = 0; phase ^= 1u; }
@@ -878,7 +897,7 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
                   const int nks = (st.K - kc * 64 + 15) >> 4;
                   const uint64_t da = da0 + (uint64_t)(kc * (ROWS * 128 / 16));
                   const uint64_t db = db0 + (uint64_t)(stage * sstep);
-                  for (int ks = 0; ks < nks; ++ks) mma_bf16_w(td, da + 2 * ks, db + 2 * ks, id, (kc | ks) ? 1u : 0u);
+                  for (int ks = 0; ks < nks; ++ks) mma_bf16_w(td, da + 2 * ks, db + 2 * ks, id, (kc | ks || fold) ? 1u : 0u);
                   tc_commit_w(BAR_EMPTY(stage));
                   if (++stage == n_stages) { stage = 0; phase ^= 1u; }
                   ++kc;
@@ -1046,22 +1065,22 @@ mlp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch, i
             const long long t_epi = kStats ? clock64() : 0;
             switch (epi) {
               case E_RELU_A:
-                epi_half<E_RELU_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_RELU_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_RELU_MASK_A:
-                epi_half<E_RELU_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_RELU_MASK_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_MASKG_A:
                 if constexpr (Op::kFused)
-                  epi_half<E_MASKG_HEAD_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                  epi_half<E_MASKG_HEAD_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 else
-                epi_half<E_MASKG_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_MASKG_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               case E_BWD_MASK_A:
-                epi_half<E_BWD_MASK_A>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_BWD_MASK_A, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
               default:
-                epi_half<E_HEAD>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
+                epi_half<E_HEAD, true>(nmine, st, c_first, r, tmem + lane_addr, a_row, my_masks, S.params + head_off, head_part, BAR_A_FREE(h), free_ph[h], S.params, mpre);
                 break;
             }
             if (kStats && threadIdx.x == EPI_WARP0 * 32) dbg_acc[7] += (unsigned long long)(clock64() - t_epi);
@@ -2026,7 +2045,8 @@ mlp_quad_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scrat
 // programs back to back), viewed as rows of 128 bytes: boxes of 128 rows
 // (16 KB, a stage) and of 8 rows (the N = 80 backward output step).
 struct Tmaps {
-  CUtensorMap box128, box8;
+  CUtensorMap box128, box8;        // the image as rows of 128 bytes: boxes of 128 and of 8 rows
+  CUtensorMap b32_128, b32_8;      // the image as rows of 32 bytes (bias chunks): boxes of 128 and of 8 rows
 };
 
 struct NetImage {
@@ -2052,15 +2072,19 @@ inline int make_weight_tmaps(const void* img, size_t bytes, Tmaps* out, std::str
     }
     enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  const cuuint64_t dims[2] = {16, (cuuint64_t)(bytes / 128)};
-  const cuuint64_t strides[1] = {128};
   const cuuint32_t estr[2] = {1, 1};
-  for (int b = 0; b < 2; ++b) {
-    const cuuint32_t box[2] = {16, b == 0 ? 128u : 8u};
-    CUresult r = enc(b == 0 ? &out->box128 : &out->box8, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(img),
-                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { *err = "cuTensorMapEncodeTiled failed"; return 4; }
+  for (int v = 0; v < 2; ++v) {         // v = 0: rows of 128 bytes, v = 1: rows of 32 bytes
+    const cuuint64_t row_u64 = v == 0 ? 16 : 4;
+    const cuuint64_t dims[2] = {row_u64, (cuuint64_t)(bytes / (row_u64 * 8))};
+    const cuuint64_t strides[1] = {row_u64 * 8};
+    for (int b = 0; b < 2; ++b) {
+      const cuuint32_t box[2] = {(cuuint32_t)row_u64, b == 0 ? 128u : 8u};
+      CUtensorMap* tm = v == 0 ? (b == 0 ? &out->box128 : &out->box8) : (b == 0 ? &out->b32_128 : &out->b32_8);
+      CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(img), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) { *err = "cuTensorMapEncodeTiled failed"; return 4; }
+    }
   }
   return 0;
 }
@@ -2069,11 +2093,16 @@ inline int make_weight_tmaps(const void* img, size_t bytes, Tmaps* out, std::str
 
 inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
 
+inline void append_bias_rows(std::vector<uint16_t>& img, int rows, const float* bias);
+
 // Append the chunks of one step: B[n][k] = src(n, k), n < N (rows), k < K.
+// half_bias (wide programs, nh = 2, bias folded): the bias chunk of each
+// N-half goes ahead of that half's K chunks.
 template <class Src>
-inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src) {
+inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src, const float* half_bias = nullptr) {
   st.img_off = (long long)img.size() * 2;
-  for (int h = 0; h < st.nh; ++h)
+  for (int h = 0; h < st.nh; ++h) {
+    if (half_bias) append_bias_rows(img, st.rows, half_bias + h * st.rows);
     for (int kc = 0; kc < st.nchunk; ++kc) {
       const size_t base = img.size();
       img.resize(base + (size_t)st.rows * 64, 0);
@@ -2086,6 +2115,7 @@ inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src) {
           std::memcpy(&img[base + off], &b, 2);
         }
     }
+  }
 }
 
 // The bias chunk of a folded step (see step_has_bias): rows x 16 bf16 (one
@@ -2094,9 +2124,12 @@ inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src) {
 // bias[n].  It follows the step's K chunks in the image.
 inline int bias_chunk_bytes(int rows) { return rows * 32; }
 inline void append_bias_chunk(std::vector<uint16_t>& img, const Step& st, const std::vector<float>& bias) {
+  append_bias_rows(img, st.rows, bias.data());
+}
+inline void append_bias_rows(std::vector<uint16_t>& img, int rows, const float* bias) {
   const size_t base = img.size();
-  img.resize(base + (size_t)st.rows * 16, 0);
-  for (int n = 0; n < st.rows; ++n) {
+  img.resize(base + (size_t)rows * 16, 0);
+  for (int n = 0; n < rows; ++n) {
     float rem = bias[n];
     for (int k = 0; k < 3; ++k) {
       const __nv_bfloat16 b = __float2bfloat16_rn(rem);
@@ -2152,7 +2185,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   Prog& P = out->host;
   std::memset(&P, 0, sizeof(P));
   P.pp = split == 1;
-  P.fold = maxh <= 128;   // quad programs
+  P.fold = maxh <= 128 || split == 2;   // quad programs (chunk after the K chunks) and wide ones (per N-half, ahead)
   P.max_hidden = maxh;
   P.k0 = wp[0];
   P.in_width = widths[0];
@@ -2173,8 +2206,8 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
     Step s = make_step(wp[l], wp[l + 1], split, l == L - 2 ? E_HEAD : E_RELU_A);
     const std::vector<float>& w = W[l];
     const int K = wp[l];
-    append_chunks(img, s, [&](int n, int k) { return w[(size_t)n * K + k]; });
-    if (P.fold) append_bias_chunk(img, s, B[l]);
+    append_chunks(img, s, [&](int n, int k) { return w[(size_t)n * K + k]; }, P.fold && split == 2 ? B[l].data() : nullptr);
+    if (P.fold && split == 1) append_bias_chunk(img, s, B[l]);
     s.bias = reinterpret_cast<const float*>(bias_off[l]);   // patched to device below
     P.fwd[l] = s;
   }
@@ -2186,8 +2219,8 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
     s.mask_layer = l;
     const std::vector<float>& w = W[l];
     const int K = wp[l];
-    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)n * K + k]; });
-    if (P.fold) append_bias_chunk(gimg, s, B[l]);
+    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)n * K + k]; }, P.fold && split == 2 ? B[l].data() : nullptr);
+    if (P.fold && split == 1) append_bias_chunk(gimg, s, B[l]);
     s.bias = reinterpret_cast<const float*>(bias_off[l]);
     P.grad[gs++] = s;
   }
@@ -2330,7 +2363,7 @@ int launch(const FieldDev& F, const std::vector<NetImage>& images, const Op& op,
     params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
   }
   const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
-  const int extra = 1024 /*align*/ + 8 * (6 + 2 * 8) + 16 + 2 * ROWS * 4 + params_bytes;
+  const int extra = 1024 /*align*/ + 8 * (6 + 2 * 8) + 16 + 2 * ROWS * 4 + params_bytes + ONES_BYTES + 256;
   int n_stages = (SMEM_LIMIT - a_bytes - extra) / chunk;
   n_stages = std::min(n_stages, 8);
   if (n_stages < 2) { *err = "bf16 engine: not enough shared memory for the weight pipeline"; return 1; }
