@@ -106,6 +106,42 @@ def test_bf16_forward_and_gradient(widths):
     assert fp32_ok(f.forward_inputs(x), ref)
 
 
+@pytest.mark.parametrize("widths", [(5, 128, 128, 128, 1), (5, 64, 96, 1), (5, 192, 256, 1), (65, 512, 512, 512, 1),
+                                    (5, 320, 448, 1), (65, 128, 128, 1)])
+def test_bf16_nonzero_biases(widths):
+    """Trained checkpoints carry biases; the BASELINE's synthetic networks have
+    none.  The <= 128-wide and > 256-wide engines fold the bias into the
+    accumulator (a bf16 hi/mid/lo bias chunk against a ones block), the
+    129..256-wide engine adds it in the epilogue: all three against the bf16
+    emulation (fp32 bias add) and the float64 reference, forward and gradient,
+    plus the fp32 engines on the same network."""
+    m = kaiming_uniform(widths, 5)
+    rng = np.random.default_rng(17)
+    m.b = [rng.normal(0.0, 0.3, size=np.shape(b)) for b in m.b]
+    f = CudaNeuralField(m, D, bounds=BOX, precision="bf16")
+    n = 2500
+    if widths[0] == 65:
+        o, d = C.query_rays(n, 4)
+        x = O.pe_encode(O.encode5(o, O.dirs_to_angles(d)))
+    else:
+        x = rng.uniform(-1, 1, (n, widths[0]))
+    y, g = f.forward_inputs(x), f.input_gradient_inputs(x)
+    ye, ge = bf16_emulation(m, x)
+    ey = np.abs(y - ye) / np.sqrt(np.mean(ye ** 2))
+    eg = np.max(np.abs(g - ge), axis=1) / np.sqrt(np.mean(ge ** 2))
+    print(f"bf16 with biases {widths}: vs emulation median {np.median(ey):.3g} max {ey.max():.3g}")
+    assert np.median(ey) <= 1e-4 and ey.max() <= 0.05
+    assert np.median(eg) <= 1e-4 and np.mean(eg > 1e-2) <= 0.10
+    ref = O.mlp_forward(onet(m), x)
+    mx, med = err_stats(y, ref)
+    assert mx <= 0.15 and med <= 0.02
+    f.set_precision("fp32")
+    assert fp32_ok(f.forward_inputs(x), ref)
+    gref = O.mlp_input_grad(onet(m), x)
+    e = np.max(np.abs(f.input_gradient_inputs(x) - gref), axis=1) / np.sqrt(np.mean(gref ** 2))
+    assert np.mean(e > 1e-4) <= 1e-3
+
+
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
 def test_pe65_query_trace_normal(prec):
     m = kaiming_uniform((65,) + (128,) * 3 + (1,), 2)
