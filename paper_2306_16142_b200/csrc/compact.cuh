@@ -157,6 +157,12 @@ __device__ __forceinline__ void st_state(unsigned long long* p, unsigned long lo
 
 constexpr int OP_IPT = 32;                  // contiguous slots per thread
 constexpr int OP_ITEMS = NT * OP_IPT;       // 8192 slots per block: a short look-back chain
+// state: nb block words, the ticket counter (state[nb]) and a finished-blocks
+// counter (state[nb + 1]).  The kernel expects them all zero and leaves them
+// all zero: the last block to finish (every block's look-back has ended by
+// then) clears them, so a call needs no memset launch ahead of it and a
+// captured graph replays without one.
+constexpr int OP_STATE_EXTRA = 2;
 
 __global__ void __launch_bounds__(NT) onepass_kernel(const uint8_t* __restrict__ flags, const uint8_t* __restrict__ sel,
                                                      int sel_val, int n, int nb, unsigned long long* state,
@@ -254,6 +260,16 @@ __global__ void __launch_bounds__(NT) onepass_kernel(const uint8_t* __restrict__
     if (rows_acc2) *rows_acc2 += (unsigned long long)pos;
     if (rows_acc3) *rows_acc3 += (unsigned long long)pos;
   }
+  // self-cleaning: this block no longer reads any state word (its look-back
+  // ended before the barrier above); the block that finishes last resets them
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&state[nb + 1], 1ull) == (unsigned long long)(nb - 1);
+  }
+  __syncthreads();
+  if (s_last)
+    for (int i = threadIdx.x; i < nb + OP_STATE_EXTRA; i += NT) state[i] = 0ull;
 }
 
 }  // namespace compact

@@ -110,6 +110,7 @@ struct ddf_field_s {
   int sm_count = 148;
   // scratch
   Buf t_acc, t_exit, alive, list, list2, blocks, small, ones;
+  Buf op_state;   // single-pass compaction state: zero between calls (compact.cuh onepass_kernel)
   Buf st_o, st_d, st_tacc, st_texit, st_t, st_thr, st_rad, st_hit, st_march, st_alive, st_obj;
   Buf pix, rng, umma_masks, st_u34, st_g3, st_gdone, st_want;
   Buf film;   // the render's accumulator: captured graphs write here, the caller's buffer gets a copy
@@ -239,14 +240,19 @@ int compact_flags(ddf_field_s* f, const uint8_t* flags, const int* obj, int n, i
                   int* count, unsigned long long* rows_acc, cudaStream_t st, const uint8_t* sel = nullptr,
                   int sel_val = 0, unsigned long long* rows_acc2 = nullptr, unsigned long long* rows_acc3 = nullptr) {
   const int nb = std::max(1, (n + compact::BLOCK_ITEMS - 1) / compact::BLOCK_ITEMS);
-  CUDA_TRY(f->blocks.ensure(std::max(sizeof(int) * nb * DDF_MAX_OBJECTS, sizeof(unsigned long long) * (nb + 1))));
+  CUDA_TRY(f->blocks.ensure(sizeof(int) * nb * DDF_MAX_OBJECTS));
   int* bc = f->blocks.as<int>();
   const int no = obj ? n_obj : 1;
   ProfScope ps(f->prof, Prof::COMPACT, st);
   if (no == 1) {   // one segment: single pass with decoupled look-back
     const int nb1 = std::max(1, (n + compact::OP_ITEMS - 1) / compact::OP_ITEMS);
-    unsigned long long* state = f->blocks.as<unsigned long long>();
-    CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb1 + 1), st));
+    // the kernel's own state buffer, zeroed when (re)allocated and left zero by every call
+    const size_t sbytes = sizeof(unsigned long long) * (nb1 + compact::OP_STATE_EXTRA);
+    if (sbytes > f->op_state.bytes) {
+      CUDA_TRY(f->op_state.ensure(std::max(sbytes, (size_t)16384)));
+      CUDA_TRY(cudaMemsetAsync(f->op_state.p, 0, f->op_state.bytes, st));
+    }
+    unsigned long long* state = f->op_state.as<unsigned long long>();
     f->prof.launches += 1;
     compact::onepass_kernel<<<nb1, compact::NT, 0, st>>>(flags, sel, sel_val, n, nb1, state, list, seg, count,
                                                           rows_acc, rows_acc2, rows_acc3);
@@ -719,7 +725,7 @@ int ddf_field_destroy(ddf_field_t f) {
   for (void* p : f->weights) cudaFree(p);
   for (auto& im : f->images) umma::free_image(&im);
   for (auto& im : f->images_x3) umma::free_image(&im);
-  Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones,
+  Buf* bufs[] = {&f->t_acc, &f->t_exit, &f->alive, &f->list, &f->list2, &f->blocks, &f->small, &f->ones, &f->op_state,
                  &f->st_o, &f->st_d, &f->st_tacc, &f->st_texit, &f->st_t, &f->st_thr, &f->st_rad,
                  &f->st_hit, &f->st_march, &f->st_alive, &f->st_obj, &f->pix, &f->rng, &f->umma_masks, &f->st_u34, &f->st_g3, &f->st_gdone, &f->st_want,
                  &f->udf_dirs, &f->udf_vals, &f->udf_pts, &f->udf_best, &f->udf_arg, &f->udf_found, &f->udf_list,
@@ -1306,10 +1312,10 @@ int ddf_compact(const uint8_t* flags, int64_t n, int32_t* list, int32_t* count, 
   }
   const int nb1 = std::max<int>(1, (int)((n + compact::OP_ITEMS - 1) / compact::OP_ITEMS));
   unsigned long long* state = nullptr;
-  const size_t bytes = sizeof(unsigned long long) * (nb1 + 1) + 2 * sizeof(int);
+  const size_t bytes = sizeof(unsigned long long) * (nb1 + compact::OP_STATE_EXTRA) + 2 * sizeof(int);
   CUDA_TRY(cudaMallocAsync((void**)&state, bytes, st));
-  CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb1 + 1), st));
-  int* seg = reinterpret_cast<int*>(state + nb1 + 1);
+  CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb1 + compact::OP_STATE_EXTRA), st));
+  int* seg = reinterpret_cast<int*>(state + nb1 + compact::OP_STATE_EXTRA);
   compact::onepass_kernel<<<nb1, compact::NT, 0, st>>>(flags, nullptr, 0, (int)n, nb1, state, list, seg, count,
                                                         nullptr, nullptr, nullptr);
   CUDA_TRY(cudaGetLastError());
