@@ -154,7 +154,8 @@ struct Prog {
   int max_chunk_bytes;
   int pp;              // 1: two-tile ping-pong program (hidden widths <= 256, one N-half per step)
   int max_hidden;      // widest padded hidden layer (<= 128: four-slot quad kernel)
-  int fold;            // 1: forward-type steps carry a bias chunk after their K chunks (pp / quad programs)
+  int fold;            // 1: forward-type steps carry a bias chunk (quad programs: after the K chunks; wide ones: per N-half, ahead)
+  int chunk_k;         // K columns per weight chunk: 64, or 32 for 256-wide ping-pong programs
   float head_b;
   const float* head_w; // fp32, padded last hidden width
   const float* params; // fp32 block: hidden-layer biases then head weights (staged in shared memory)
@@ -343,6 +344,27 @@ __device__ __forceinline__ void mma_k64_w(uint32_t tmem_d, uint32_t da, uint32_t
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t}" ::"r"(tmem_d),
       "r"(da), "r"(db), "r"(id), "r"(acc), "n"(SDESC_HI)
+      : "memory");
+}
+// One 32-wide K chunk of a ping-pong program (two K = 16 MMAs) and the commit
+// that frees its stage: A in the 128-byte swizzle (the A tile), B in the
+// 64-byte swizzle (SBO 512 B).
+constexpr uint32_t SDESC64B_HI = (uint32_t)((512 >> 4) | (1u << 14) | (4u << 29));
+__device__ __forceinline__ void mma_k32_commit_w(uint32_t tmem_d, uint32_t da, uint32_t db, uint32_t id,
+                                                 uint32_t acc, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, e;\n\t.reg .b32 x1, y1;\n\t"
+      ".reg .b64 a0, a1, b0, b1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, %3, %3;\n\t"
+      "add.u32 x1, %1, 2;\n\tadd.u32 y1, %2, 2;\n\t"
+      "mov.b64 a0, {%1, %6};\n\tmov.b64 a1, {x1, %6};\n\t"
+      "mov.b64 b0, {%2, %7};\n\tmov.b64 b1, {y1, %7};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(tmem_d),
+      "r"(da), "r"(db), "r"(id), "r"(acc), "r"(bar), "n"(SDESC_HI), "n"(SDESC64B_HI)
       : "memory");
 }
 __device__ __forceinline__ void mma_bf16_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -1359,11 +1381,12 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
         for (int j = j0; j < j1; ++j) {
           const Prog* P = reinterpret_cast<const Prog*>(F.net[j].wimg_fwd);
           const int ns = uni(__ldg(Op::kGrad ? &P->n_grad : &P->n_fwd));
+          const bool k32 = uni(__ldg(&P->chunk_k)) == 32;   // 256-wide programs: chunks of 32 K columns
           for (int s = 0; s < ns; ++s) {
             Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
             uni_step(st);
             const uint32_t id = idesc(st.rows);
-            const int nfull = st.K >> 6;
+            const int nfull = k32 ? st.K >> 5 : st.K >> 6;   // chunks of two / four K = 16 MMAs
 #pragma unroll
             for (int sl = 0; sl < 2; ++sl) {
               // this slot's A tile (and its TMEM columns) are ready
@@ -1376,17 +1399,28 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
               for (int kc = 0; kc < st.nchunk; ++kc) {
                 mbar_wait_u(bars_u + 8u * (uint32_t)(4 + stage), phase);
                 tc_after_sync();
-                const uint32_t da = da_lo + (uint32_t)(kc * (ROWS * 128 / 16));
                 const uint32_t db = db0_lo + (uint32_t)stage * sstep;
                 const uint32_t bar_empty = bars_u + 8u * (uint32_t)(4 + nst + stage);
-                if (kc < nfull) {
-                  mma_k64_commit_w(td, da, db, id, kc ? 1u : 0u, bar_empty);
+                if (k32) {
+                  // chunk kc = A columns [32 kc, 32 kc + 32): k-block kc / 2 of the A tile, its half kc & 1
+                  const uint32_t da = da_lo + (uint32_t)((kc >> 1) * (ROWS * 128 / 16) + (kc & 1) * 4);
+                  if (kc < nfull) {
+                    mma_k32_commit_w(td, da, db, id, kc ? 1u : 0u, bar_empty);
+                  } else {   // a last chunk of 16 K columns (the input layer)
+                    mma_bf16_w(td, ((uint64_t)SDESC_HI << 32) | da, ((uint64_t)SDESC64B_HI << 32) | db, id, kc ? 1u : 0u);
+                    tc_commit_w(bar_empty);
+                  }
                 } else {
-                  const int nks = (st.K - kc * 64 + 15) >> 4;
-                  for (int ks = 0; ks < nks; ++ks)
-                    mma_bf16_w(td, ((uint64_t)SDESC_HI << 32) | (da + 2 * ks), ((uint64_t)SDESC_HI << 32) | (db + 2 * ks), id,
-                               (kc | ks) ? 1u : 0u);
-                  tc_commit_w(bar_empty);
+                  const uint32_t da = da_lo + (uint32_t)(kc * (ROWS * 128 / 16));
+                  if (kc < nfull) {
+                    mma_k64_commit_w(td, da, db, id, kc ? 1u : 0u, bar_empty);
+                  } else {
+                    const int nks = (st.K - kc * 64 + 15) >> 4;
+                    for (int ks = 0; ks < nks; ++ks)
+                      mma_bf16_w(td, ((uint64_t)SDESC_HI << 32) | (da + 2 * ks), ((uint64_t)SDESC_HI << 32) | (db + 2 * ks), id,
+                                 (kc | ks) ? 1u : 0u);
+                    tc_commit_w(bar_empty);
+                  }
                 }
                 if (++stage == nst) { stage = 0; phase ^= 1u; }
               }
@@ -2098,20 +2132,28 @@ inline void append_bias_rows(std::vector<uint16_t>& img, int rows, const float* 
 // Append the chunks of one step: B[n][k] = src(n, k), n < N (rows), k < K.
 // half_bias (wide programs, nh = 2, bias folded): the bias chunk of each
 // N-half goes ahead of that half's K chunks.
+// ck = 64: chunks of 64 K columns, rows of 128 B in the 128-byte swizzle.
+// ck = 32 (ping-pong programs): chunks of 32 K columns, rows of 64 B in the
+// 64-byte swizzle (16-byte unit u of row n at u ^ ((n >> 1) & 3)): half the
+// stage size, so the weight ring holds five stages beside the two A tiles
+// instead of two.
 template <class Src>
-inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src, const float* half_bias = nullptr) {
+inline void append_chunks(std::vector<uint16_t>& img, Step& st, Src src, const float* half_bias = nullptr,
+                          int ck = 64) {
   st.img_off = (long long)img.size() * 2;
   for (int h = 0; h < st.nh; ++h) {
     if (half_bias) append_bias_rows(img, st.rows, half_bias + h * st.rows);
     for (int kc = 0; kc < st.nchunk; ++kc) {
       const size_t base = img.size();
-      img.resize(base + (size_t)st.rows * 64, 0);
+      img.resize(base + (size_t)st.rows * ck, 0);
       for (int n = 0; n < st.rows; ++n)
-        for (int k = 0; k < 64; ++k) {
-          const int gn = h * st.rows + n, gk = kc * 64 + k;
+        for (int k = 0; k < ck; ++k) {
+          const int gn = h * st.rows + n, gk = kc * ck + k;
           const float v = (gk < st.K) ? src(gn, gk) : 0.f;
           __nv_bfloat16 b = __float2bfloat16_rn(v);
-          const size_t off = (size_t)(n >> 3) * 512 + (size_t)(n & 7) * 64 + (size_t)((((k >> 3) ^ (n & 7)) << 3) + (k & 7));
+          const size_t off = ck == 64
+              ? (size_t)(n >> 3) * 512 + (size_t)(n & 7) * 64 + (size_t)((((k >> 3) ^ (n & 7)) << 3) + (k & 7))
+              : (size_t)n * 32 + (size_t)((((k >> 3) ^ ((n >> 1) & 3)) << 3) + (k & 7));
           std::memcpy(&img[base + off], &b, 2);
         }
     }
@@ -2140,12 +2182,12 @@ inline void append_bias_rows(std::vector<uint16_t>& img, int rows, const float* 
   }
 }
 
-inline Step make_step(int K, int N, int nh, int epi) {
+inline Step make_step(int K, int N, int nh, int epi, int ck = 64) {
   Step s{};
   s.K = K; s.N = N; s.nh = nh; s.epi = epi;
   s.rows = N / nh;
-  s.nchunk = (K + 63) / 64;
-  s.chunk_bytes = s.rows * 128;
+  s.nchunk = (K + ck - 1) / ck;
+  s.chunk_bytes = s.rows * ck * 2;
   s.mask_layer = -1;
   s.bias = nullptr;
   return s;
@@ -2185,6 +2227,12 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   Prog& P = out->host;
   std::memset(&P, 0, sizeof(P));
   P.pp = split == 1;
+  // Ping-pong programs at 256 wide: 32-column chunks.  With 64-column (32 KB) chunks only two stages fit
+  // beside the two 64 KB A tiles and the weight stream is latency-starved; 16 KB stages give five
+  // (5->8x256 forward 1300 -> 1401 TF/s).  At 192 wide five 24 KB stages fit already and the extra
+  // barrier round per two MMAs costs more than it hides (788 -> 659 TF/s), so those keep 64.
+  const int ck = (split == 1 && maxh > 192) ? 32 : 64;
+  P.chunk_k = ck;
   P.fold = maxh <= 128 || split == 2;   // quad programs (chunk after the K chunks) and wide ones (per N-half, ahead)
   P.max_hidden = maxh;
   P.k0 = wp[0];
@@ -2203,10 +2251,10 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   // forward program: hidden layers 0..L-2, the last one fused with the head
   P.n_fwd = L - 1;
   for (int l = 0; l < L - 1; ++l) {
-    Step s = make_step(wp[l], wp[l + 1], split, l == L - 2 ? E_HEAD : E_RELU_A);
+    Step s = make_step(wp[l], wp[l + 1], split, l == L - 2 ? E_HEAD : E_RELU_A, ck);
     const std::vector<float>& w = W[l];
     const int K = wp[l];
-    append_chunks(img, s, [&](int n, int k) { return w[(size_t)n * K + k]; }, P.fold && split == 2 ? B[l].data() : nullptr);
+    append_chunks(img, s, [&](int n, int k) { return w[(size_t)n * K + k]; }, P.fold && split == 2 ? B[l].data() : nullptr, ck);
     if (P.fold && split == 1) append_bias_chunk(img, s, B[l]);
     s.bias = reinterpret_cast<const float*>(bias_off[l]);   // patched to device below
     P.fwd[l] = s;
@@ -2215,11 +2263,11 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   std::vector<uint16_t> gimg;
   int gs = 0;
   for (int l = 0; l < L - 1; ++l) {
-    Step s = make_step(wp[l], wp[l + 1], split, l == L - 2 ? E_MASKG_A : E_RELU_MASK_A);
+    Step s = make_step(wp[l], wp[l + 1], split, l == L - 2 ? E_MASKG_A : E_RELU_MASK_A, ck);
     s.mask_layer = l;
     const std::vector<float>& w = W[l];
     const int K = wp[l];
-    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)n * K + k]; }, P.fold && split == 2 ? B[l].data() : nullptr);
+    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)n * K + k]; }, P.fold && split == 2 ? B[l].data() : nullptr, ck);
     if (P.fold && split == 1) append_bias_chunk(gimg, s, B[l]);
     s.bias = reinterpret_cast<const float*>(bias_off[l]);
     P.grad[gs++] = s;
@@ -2227,11 +2275,11 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   // backward: layer l maps d z_l (width wp[l+1]) to d h_l (width wp[l]) with B[n][k] = W_l[k][n]
   for (int l = L - 2; l >= 0; --l) {
     const bool last = l == 0;
-    Step s = make_step(wp[l + 1], wp[l], last ? 1 : split, last ? E_BWD_OUT : E_BWD_MASK_A);
+    Step s = make_step(wp[l + 1], wp[l], last ? 1 : split, last ? E_BWD_OUT : E_BWD_MASK_A, ck);
     s.mask_layer = l - 1;
     const std::vector<float>& w = W[l];
     const int Kin = wp[l];
-    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)k * Kin + n]; });
+    append_chunks(gimg, s, [&](int n, int k) { return w[(size_t)k * Kin + n]; }, nullptr, ck);
     P.grad[gs++] = s;
   }
   P.n_grad = gs;
