@@ -1161,7 +1161,7 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
                                            uint32_t* my_masks, const float* head_w, float& head_part,
                                            const float* sparams) {
   const int r7 = r & 7;
-  const uint32_t bias_s = smem_u32(sparams) + 4u * (uint32_t)(size_t)st.bias;
+  (void)sparams;
   const uint32_t head_s = smem_u32(head_w);
   uint32_t rgb[2][32];
   DDF_TMEM_LD32(tmem_row + (uint32_t)c_first, rgb[0]);
@@ -1173,15 +1173,11 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
     const int c = c_first + i * STRIDE;
     if (i + 1 < NM) DDF_TMEM_LD32(tmem_row + (uint32_t)(c + STRIDE), rgb[(i + 1) & 1]);
     const uint32_t(&rg)[32] = rgb[i & 1];
-    float4 bq[8];
+    // no bias here: it is already in the accumulator (step_has_bias)
     const uint32_t mq = mq_next;
-    if constexpr (EPI != E_BWD_MASK_A) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) bq[k] = ld_shared_f4(bias_s + 4u * (uint32_t)(c + 4 * k));
-    } else {
+    if constexpr (EPI == E_BWD_MASK_A) {
       if (i + 1 < NM) mq_next = my_masks[(st.mask_layer * 16 + ((c + STRIDE) >> 5)) * ROWS + r];
     }
-    const float* bf = reinterpret_cast<const float*>(bq);
     uint32_t pkd[16];
     if constexpr (EPI == E_BWD_MASK_A) {
 #pragma unroll
@@ -1191,22 +1187,22 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
     } else if constexpr (EPI == E_RELU_A) {
 #pragma unroll
       for (int e = 0; e < 16; ++e)
-        pkd[e] = pack_bf16_relu(__uint_as_float(rg[2 * e]) + bf[2 * e], __uint_as_float(rg[2 * e + 1]) + bf[2 * e + 1]);
+        pkd[e] = pack_bf16_relu(__uint_as_float(rg[2 * e]), __uint_as_float(rg[2 * e + 1]));
     } else if constexpr (EPI == E_HEAD) {
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
         const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e]) + bf[e], 0.f), hw.x, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]) + bf[e + 1], 0.f), hw.y, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]) + bf[e + 2], 0.f), hw.z, head_part);
-        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 3]) + bf[e + 3], 0.f), hw.w, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e]), 0.f), hw.x, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]), 0.f), hw.y, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]), 0.f), hw.z, head_part);
+        head_part = fmaf(fmaxf(__uint_as_float(rg[e + 3]), 0.f), hw.w, head_part);
       }
     } else {
       uint32_t mw = 0u;
       float v[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
-        const float z = __uint_as_float(rg[e]) + bf[e];
+        const float z = __uint_as_float(rg[e]);
         mw |= (z > 0.f ? 1u : 0u) << e;
         v[e] = z;
       }
@@ -1300,6 +1296,8 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
   float* red = reinterpret_cast<float*>(tmem_slot + 4);           // [2 slots][2 subs][128]
   float* sparams = red + 4 * ROWS;                                // [2 slots][params_bytes/4]
   const int pfl = params_bytes >> 2;
+  // the bias fold's constant A block, aligned to its 256-byte swizzle atom
+  uint8_t* ones = reinterpret_cast<uint8_t*>(((uintptr_t)(sparams + 2 * pfl) + 255) & ~(uintptr_t)255);
 
   const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t bar0 = smem_u32(bars);
@@ -1323,6 +1321,8 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  write_ones_block(ones, threadIdx.x, blockDim.x);
+  fence_async_smem();
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
@@ -1345,12 +1345,14 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
           const uint8_t* img = Op::kGrad ? P->img_grad : P->img_fwd;
           for (int s = 0; s < ns; ++s) {
             const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
+            const int nck = st.nchunk + (step_has_bias(st.epi) ? 1 : 0);   // + the bias chunk (rows x 32 B)
             for (int sl = 0; sl < 2; ++sl) {
               const uint8_t* src = img + st.img_off;
-              for (int c = 0; c < st.nchunk; ++c) {
+              for (int c = 0; c < nck; ++c) {
+                const uint32_t bytes = c < st.nchunk ? (uint32_t)st.chunk_bytes : (uint32_t)(st.rows * 32);
                 mbar_wait(BAR_EMPTY(stage), phase ^ 1u);
-                mbar_expect_tx(BAR_FULL(stage), (uint32_t)st.chunk_bytes);
-                bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, (uint32_t)st.chunk_bytes, BAR_FULL(stage));
+                mbar_expect_tx(BAR_FULL(stage), bytes);
+                bulk_g2s(st_base + (uint32_t)(stage * stage_bytes), src, bytes, BAR_FULL(stage));
                 src += st.chunk_bytes;
                 if (++stage == n_stages) { stage = 0; phase ^= 1u; }
               }
@@ -1370,6 +1372,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
       const uint32_t a0_lo = uni(sdesc_lo(a_base0)), db0_lo = uni(sdesc_lo(st_base));
       const uint32_t a_step = uni((uint32_t)a_bytes >> 4), sstep = uni((uint32_t)stage_bytes >> 4);
       const int nst = uni(n_stages), pairs_u = uni(pairs);
+      const uint32_t ones_lo = uni(sdesc_lo(smem_u32(ones)));
       TraceCursor tcur{1, 0};
       for (int pr = blockIdx.x; pr < pairs_u; pr += gridDim.x) {
         int j0, j1, base, nv;
@@ -1422,6 +1425,13 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
                     tc_commit_w(bar_empty);
                   }
                 }
+                if (++stage == nst) { stage = 0; phase ^= 1u; }
+              }
+              if (step_has_bias(st.epi)) {   // D += bias (the step's last chunk, see step_has_bias)
+                mbar_wait_u(bars_u + 8u * (uint32_t)(4 + stage), phase);
+                tc_after_sync();
+                mma_bias_w(td, ones_lo, db0_lo + (uint32_t)stage * sstep, id);
+                tc_commit_w(bars_u + 8u * (uint32_t)(4 + nst + stage));
                 if (++stage == nst) { stage = 0; phase ^= 1u; }
               }
               tc_commit_w(bars_u + 8u * (uint32_t)(2 + sl));
@@ -2233,7 +2243,7 @@ inline int build_image(const int32_t* widths, int32_t n_widths, const double* we
   // barrier round per two MMAs costs more than it hides (788 -> 659 TF/s), so those keep 64.
   const int ck = (split == 1 && maxh > 192) ? 32 : 64;
   P.chunk_k = ck;
-  P.fold = maxh <= 128 || split == 2;   // quad programs (chunk after the K chunks) and wide ones (per N-half, ahead)
+  P.fold = 1;   // every bf16 program: quad / ping-pong (chunk after the K chunks) and wide (per N-half, ahead)   // quad programs (chunk after the K chunks) and wide ones (per N-half, ahead)
   P.max_hidden = maxh;
   P.k0 = wp[0];
   P.in_width = widths[0];
@@ -2335,7 +2345,7 @@ int launch_pp(const FieldDev& F, const std::vector<NetImage>& images, const Op& 
     params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
   }
   const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
-  const int extra = 1024 + 8 * (4 + 2 * 8) + 16 + 4 * ROWS * 4 + 2 * params_bytes;
+  const int extra = 1024 + 8 * (4 + 2 * 8) + 16 + 4 * ROWS * 4 + 2 * params_bytes + ONES_BYTES + 256;
   int n_stages = std::min(8, (SMEM_LIMIT - 2 * a_bytes - extra) / chunk);
   if (n_stages < 2) { *err = "bf16 ping-pong engine: not enough shared memory"; return 1; }
   const size_t smem = 2 * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
