@@ -1162,7 +1162,6 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
                                            const float* sparams) {
   const int r7 = r & 7;
   (void)sparams;
-  const uint32_t head_s = smem_u32(head_w);
   uint32_t rgb[2][32];
   DDF_TMEM_LD32(tmem_row + (uint32_t)c_first, rgb[0]);
   uint32_t mq_next = 0u;
@@ -1191,7 +1190,7 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
     } else if constexpr (EPI == E_HEAD) {
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
-        const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
+        const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w + c + e));
         head_part = fmaf(fmaxf(__uint_as_float(rg[e]), 0.f), hw.x, head_part);
         head_part = fmaf(fmaxf(__uint_as_float(rg[e + 1]), 0.f), hw.y, head_part);
         head_part = fmaf(fmaxf(__uint_as_float(rg[e + 2]), 0.f), hw.z, head_part);
@@ -1213,7 +1212,7 @@ __device__ __forceinline__ void epi_direct(const Step& st, int c_first, int r, u
       } else {
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
-          const float4 hw = ld_shared_f4(head_s + 4u * (uint32_t)(c + e));
+          const float4 hw = __ldg(reinterpret_cast<const float4*>(head_w + c + e));
           v[e] = ((mw >> e) & 1u) ? hw.x : 0.f;
           v[e + 1] = ((mw >> (e + 1)) & 1u) ? hw.y : 0.f;
           v[e + 2] = ((mw >> (e + 2)) & 1u) ? hw.z : 0.f;
@@ -1294,10 +1293,9 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)n_stages * stage_bytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * n_stages);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);           // [2 slots][2 subs][128]
-  float* sparams = red + 4 * ROWS;                                // [2 slots][params_bytes/4]
-  const int pfl = params_bytes >> 2;
+  (void)params_bytes;   // nothing of a network's params is staged: biases are folded, head weights read in place
   // the bias fold's constant A block, aligned to its 256-byte swizzle atom
-  uint8_t* ones = reinterpret_cast<uint8_t*>(((uintptr_t)(sparams + 2 * pfl) + 255) & ~(uintptr_t)255);
+  uint8_t* ones = reinterpret_cast<uint8_t*>(((uintptr_t)(red + 4 * ROWS) + 255) & ~(uintptr_t)255);
 
   const int warp = uni((int)(threadIdx.x >> 5)), lane = threadIdx.x & 31;   // warp index, provably warp-uniform
   const uint32_t bar0 = smem_u32(bars);
@@ -1497,15 +1495,6 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
         double u[2][5];
 #pragma unroll
         for (int sl = 0; sl < 2; ++sl) {
-          // params of this network for the slot (the slot's previous network is done)
-          {
-            const int nf = __ldg(&P->params_floats);
-            const float4* src = reinterpret_cast<const float4*>(P->params);
-            float4* dst = reinterpret_cast<float4*>(sparams + sl * pfl);
-            named_sync(1, N_EPI_WARPS * 32);
-            for (int i = threadIdx.x - EPI_WARP0 * 32; i < (nf >> 2); i += N_EPI_WARPS * 32) dst[i] = __ldg(src + i);
-            named_sync(1, N_EPI_WARPS * 32);
-          }
           for (int e = 0; e < 5; ++e) u[sl][e] = 0.0;
           if constexpr (!Op::kRaw) {
             if (valid[sl]) row_u(F, j, pos[sl], az[sl], pol[sl], u[sl]);
@@ -1571,7 +1560,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
             }
             const uint32_t a_row = a_base0 + (uint32_t)(sl * a_bytes) + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
             const int nm = (st.rows - sub * 32 + 63) >> 6;
-            const float* sp = sparams + sl * pfl;
+            const float* sp = P->params;   // global: only the head weights are read (bias folded)
             switch (epi) {
               case E_RELU_A: epi_direct_n<E_RELU_A>(nm, st, sub * 32, r, tmem_row, a_row, my_masks, sp + head_off, head_part[sl], sp); break;
               case E_RELU_MASK_A: epi_direct_n<E_RELU_MASK_A>(nm, st, sub * 32, r, tmem_row, a_row, my_masks, sp + head_off, head_part[sl], sp); break;
@@ -2345,7 +2334,7 @@ int launch_pp(const FieldDev& F, const std::vector<NetImage>& images, const Op& 
     params_bytes = std::max(params_bytes, images[j].host.params_floats * 4);
   }
   const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
-  const int extra = 1024 + 8 * (4 + 2 * 8) + 16 + 4 * ROWS * 4 + 2 * params_bytes + ONES_BYTES + 256;
+  const int extra = 1024 + 8 * (4 + 2 * 8) + 16 + 4 * ROWS * 4 + ONES_BYTES + 256;
   int n_stages = std::min(8, (SMEM_LIMIT - 2 * a_bytes - extra) / chunk);
   if (n_stages < 2) { *err = "bf16 ping-pong engine: not enough shared memory"; return 1; }
   const size_t smem = 2 * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
