@@ -887,7 +887,7 @@ def main():
     # --set full capture of this workload (profiles/), next to the
     # algorithmic path-state bytes of that launch
     ncu_path = None
-    for ver in ("r2_%s_ncu_v5", "r2_%s_ncu_v3", "r1_%s_ncu_v11"):
+    for ver in ("r2_%s_ncu_v6", "r2_%s_ncu_v3", "r1_%s_ncu_v11"):
         cand = os.path.join(ROOT, "profiles", (ver % name) + ".json")
         if os.path.exists(cand):
             ncu_path = cand
