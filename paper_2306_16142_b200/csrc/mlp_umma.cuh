@@ -212,7 +212,12 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
 }
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+#ifdef DDF_EXP_NOFENCE
+// timing experiment only (racy): what does the generic -> async proxy fence cost the row warps?
+__device__ __forceinline__ void fence_async_smem() {}
+#else
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+#endif
 
 // K-major, 128-byte swizzled canonical layout: 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
