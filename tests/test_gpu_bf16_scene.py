@@ -106,8 +106,8 @@ def test_bf16_forward_and_gradient(widths):
     assert fp32_ok(f.forward_inputs(x), ref)
 
 
-@pytest.mark.parametrize("widths", [(5, 128, 128, 128, 1), (5, 64, 96, 1), (5, 192, 256, 1), (65, 512, 512, 512, 1),
-                                    (5, 320, 448, 1), (65, 128, 128, 1)])
+@pytest.mark.parametrize("widths", [(5, 128, 128, 128, 1), (5, 64, 96, 1), (5, 192, 256, 1), (5, 160, 192, 1),
+                                    (65, 512, 512, 512, 1), (5, 320, 448, 1), (65, 128, 128, 1)])
 def test_bf16_nonzero_biases(widths):
     """Trained checkpoints carry biases; the BASELINE's synthetic networks have
     none.  The <= 128-wide and > 256-wide engines fold the bias into the
@@ -203,6 +203,32 @@ def test_scene_composite(prec):
     cos = np.clip(np.einsum("ij,ij->i", n, nr), -1, 1)
     ang_err = np.degrees(np.arccos(cos))
     assert (ang_err.max() < 0.05) if prec == "fp32" else (np.median(ang_err) < 5.0)
+
+
+@pytest.mark.parametrize("hidden", [96, 256])
+def test_scene_composite_nonzero_biases(hidden):
+    """Several networks per tile with biases in every layer: the quad (96) and
+    ping-pong (256) engines switch network between tiles' layers, each with
+    its own folded bias chunks and head weights read in place."""
+    rng = np.random.default_rng(23)
+    ms = [kaiming_uniform((65, hidden, hidden, 1), s) for s in range(30, 33)]
+    for m in ms:
+        m.b = [rng.normal(0.0, 0.25, size=np.shape(b)) for b in m.b]
+    centers, scale, albedos = C.scene_layout()
+    centers, albedos = centers[:3], albedos[:3]
+    f = CudaNeuralField.scene(ms, centers, scale, albedos, D, bounds=C.SCENE_BOX, precision="bf16")
+    of = O.Field([onet(m) for m in ms], D, bounds=C.SCENE_BOX, centers=centers, scale=scale, albedos=albedos)
+    o, d = C.query_rays(3000, 12)
+    o = o * 3.0
+    pred, t, hit, obj = f.query_raw(o, d)
+    ang = O.dirs_to_angles(O.angles_to_dirs(O.dirs_to_angles(d)))
+    pref, oref = of.predict(o, ang)
+    assert err_stats(pred, pref)[0] <= 0.15 and err_stats(pred, pref)[1] <= 0.02
+    assert (obj == oref).mean() >= 0.9
+    f.set_precision("fp32")
+    p32, _, _, o32 = f.query_raw(o, d)
+    assert fp32_ok(p32, pref)
+    assert (o32 == oref).mean() >= 0.999
 
 
 def _cam(w, h):
