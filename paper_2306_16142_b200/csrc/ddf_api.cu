@@ -640,6 +640,7 @@ int ddf_field_add_network(ddf_field_t f, const int32_t* widths, int32_t n_widths
   N.encoding = encoding;
   for (int k = 0; k < 3; ++k) N.center[k] = center ? center[k] : 0.0;
   N.scale = scale;
+  N.inv_scale = 1.0 / scale;
   N.albedo = albedo;
   std::vector<int> wp(L + 1);
   for (int l = 0; l < L; ++l) wp[l] = pad16(widths[l]);

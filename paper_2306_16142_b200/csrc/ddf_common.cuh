@@ -155,6 +155,7 @@ struct NetDev {
   int encoding;                    // Encoding
   double center[3];                // EXTENSION (config 5): object translation
   double scale;                    // EXTENSION: uniform object scale
+  double inv_scale;                // 1 / scale, for the bf16 engines' input encoding (row_u_bf16)
   double albedo;                   // EXTENSION: per-object albedo
   // fp32 engine: row-major (out, in) effective weights and their transposes
   const float* w[DDF_MAX_LAYERS];

@@ -59,6 +59,23 @@ __device__ __forceinline__ void row_u(const FieldDev& F, int j, const double* po
   u[4] = u4;
 }
 
+// The same for the bf16 engines: the object-local position by a multiply with
+// 1 / scale instead of three f64 divisions (one f64 ulp apart, far below the
+// bf16 rounding of the encoded inputs).  The divisions were a measurable part
+// of the ~2 K-cycle encoding at each of config 5's eight network boundaries
+// per tile; the fp32 engines keep row_u.
+__device__ __forceinline__ void row_u_bf16(const FieldDev& F, int j, const double* pos, double u3, double u4,
+                                           double u[5]) {
+  if (F.composite) {
+    const NetDev& n = F.net[j];
+    for (int c = 0; c < 3; ++c) u[c] = dmul(dsub(pos[c], n.center[c]), n.inv_scale);
+  } else {
+    for (int c = 0; c < 3; ++c) u[c] = pos[c];
+  }
+  u[3] = u3;
+  u[4] = u4;
+}
+
 // encoded angle inputs of a unit direction (field.py:77-82 + neural.py:36-37)
 __device__ __forceinline__ void dir_u34(d3 d, double& u3, double& u4) {
   double az, pol;

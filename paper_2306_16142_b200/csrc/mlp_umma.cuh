@@ -1502,7 +1502,7 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
         for (int sl = 0; sl < 2; ++sl) {
           for (int e = 0; e < 5; ++e) u[sl][e] = 0.0;
           if constexpr (!Op::kRaw) {
-            if (valid[sl]) row_u(F, j, pos[sl], az[sl], pol[sl], u[sl]);
+            if (valid[sl]) row_u_bf16(F, j, pos[sl], az[sl], pol[sl], u[sl]);
           }
           const uint32_t a_slot = a_base0 + (uint32_t)(sl * a_bytes);
           if constexpr (!Op::kRaw) {
@@ -1529,6 +1529,15 @@ mlp_pp_kernel(const FieldDev F, const Op op, uint32_t* __restrict__ mask_scratch
         for (int s = 0; s < ns; ++s) {
           const Step st = load_step(Op::kGrad ? &P->grad[s] : &P->fwd[s]);
           const int epi = st.epi;
+          // the head weights of this warp's columns (read in place by the HEAD / MASKG epilogue) into
+          // L1 while the step's MMAs run: a first touch costs an L2 round trip per 32-column chunk
+          if (epi == E_HEAD || epi == E_MASKG_A) {
+            const int nm = (st.rows - sub * 32 + 63) >> 6;
+            if (lane < 8 * nm) {
+              const float* hp = P->params + head_off + sub * 32 + 64 * (lane >> 3) + 4 * (lane & 7);
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(hp));
+            }
+          }
 #pragma unroll
           for (int sl = 0; sl < 2; ++sl) {
             tcur.ev(trc, 17, s * 2 + sl, 0);                     // 17: wait for the accumulator begins
