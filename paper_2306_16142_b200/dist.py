@@ -120,11 +120,13 @@ def balanced_owners_distributed(backend, camera, config, world: int, tile: int |
     return balanced_tile_owners(cost.cpu().numpy(), world), time.perf_counter() - t0
 
 
-def reduce_film(accum, group=None, dst: int = 0):
+def reduce_film(accum, group=None, dst: int = 0, force_collective: bool = False):
     """Sum the per-rank films onto rank ``dst`` in place (NCCL reduce; gloo
-    reduces a host copy).  Exact: every pixel has one non-zero term."""
+    reduces a host copy).  Exact: every pixel has one non-zero term.  A
+    one-rank group skips the collective unless ``force_collective`` (tests
+    run the NCCL reduce itself on the one GPU of the test box)."""
     import torch.distributed as dist
-    if dist.get_world_size(group) == 1:
+    if dist.get_world_size(group) == 1 and not force_collective:
         return accum
     if _collective_device(group) == "cpu" and accum.is_cuda:
         host = accum.cpu()

@@ -76,6 +76,37 @@ def test_two_rank_render_equals_single_rank(precision, balance, tile):
         assert all(p is not None and p > 0 for _, _, _, p in got)
 
 
+def _nccl_worker(port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    from paper_2306_16142_b200 import render as R
+    from paper_2306_16142_b200.dist import balanced_owners_distributed, reduce_film, tile_config
+    f, cam, cfg = _setup("bf16", tile=32)
+    accum, _ = R.render_path_device(f, cam, tile_config(cfg, 0, 1))
+    want = accum.clone()
+    reduce_film(accum, force_collective=True)          # ncclReduce of the float64 film
+    table, pilot_s = balanced_owners_distributed(f, cam, cfg, 1)   # ncclAllReduce of the cost vector
+    torch.cuda.synchronize()
+    out.put((bool(torch.equal(accum, want)), sorted(set(int(x) for x in table)), float(pilot_s), dist.get_backend()))
+    dist.destroy_process_group()
+
+
+def test_nccl_collectives_on_one_rank():
+    """The box has one GPU and NCCL refuses two ranks on one device, so the
+    multi-GPU path's two collectives (the float64 film reduce and the pilot's
+    cost all-reduce) run here over NCCL in a one-rank group: the calls, dtypes
+    and device placement the N-GPU run makes, with nothing to sum."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    same, owners, pilot_s, backend = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert backend == "nccl" and same and owners == [0] and pilot_s > 0
+
+
 def test_tile_owner_table_partitions_film_exactly():
     """Three ranks under a pilot-balanced table (and a hand-made one): the
     per-rank films are disjoint and sum bit-exactly to the 1-rank film; a bad
