@@ -947,7 +947,8 @@ def main():
                        "tiles": cfg.tile, "parallelism": f"tiles{world}" if world > 1 else "single",
                        "tile_assignment": (("pilot-balanced (LPT)" if cfg.tile_owner is not None else "round-robin")
                                            if world > 1 else None),
-                       "collective": "film sum-reduce to rank 0 (NCCL), inside the step" if world > 1 else None,
+                       "collective": (f"film sum-reduce to rank 0 ({args.dist_backend.upper() if args.dist_backend != 'nccl' else 'NCCL'}), inside the step"
+                                 if world > 1 else None),
                        "l2": "flushed (256 MB write) between timed steps"},
             "ddf_queries_per_s": stp["forward_rows"] / (ms / 1e3),
             "gradient_rows_per_s": stp["gradient_rows"] / (ms / 1e3),
