@@ -2375,7 +2375,8 @@ int launch_quad(const FieldDev& F, const std::vector<NetImage>& images, const Op
   const int a_bytes = ROWS * pad_to(kmax, 64) * 2;
   const int extra = 1024 + 8 * (2 * NSL + 2 * 8) + 16 + params_bytes + ONES_BYTES + 256;
   int n_stages = std::min(8, (SMEM_LIMIT - NSL * a_bytes - extra) / chunk);
-  if (n_stages < 2) { *err = "bf16 quad engine: not enough shared memory"; return 1; }
+  // a layer's chunks (at most two K chunks and the bias chunk) stay in the ring until the last slot has read them
+  if (n_stages < 4) { *err = "bf16 quad engine: not enough shared memory"; return 1; }
   const size_t smem = NSL * (size_t)a_bytes + (size_t)n_stages * chunk + extra;
   auto kern = mlp_quad_kernel<Op, NSL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
